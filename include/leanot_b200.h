@@ -1,0 +1,172 @@
+/*
+ * leanot_b200.h -- C ABI of the B200-native DXG hot path (libleanot_b200.so).
+ *
+ * The reference (`leanot`, /root/reference/pkg/src/leanot) is pure Python/NumPy;
+ * its only extension point on this path is the CostKernel plugin protocol
+ * (core.py:167-192) consumed by the streamed sweeps of dxg.py / barycenter.py.
+ * This library replaces those sweeps and the O(n) updates.  Every entry point:
+ *   - takes raw DEVICE pointers + sizes (no torch types), plus a cudaStream_t
+ *     (passed as void*; NULL = legacy default stream), and is stream-ordered;
+ *   - never allocates persistent memory and never frees caller memory;
+ *   - returns 0 on success, or a negative LEANOT_E* code with a message
+ *     retrievable from leanot_last_error() (thread-local); no C++ exception
+ *     crosses the boundary.  Invalid arguments are LEANOT_EINVAL, which the
+ *     Python layer maps to ValueError exactly where the reference raises it.
+ * All arithmetic is IEEE binary64.
+ */
+#ifndef LEANOT_B200_H
+#define LEANOT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LEANOT_ABI_VERSION 1
+
+#define LEANOT_OK 0
+#define LEANOT_EINVAL (-1)
+#define LEANOT_ECUDA (-2)
+#define LEANOT_EINTERNAL (-3)
+
+#define LEANOT_MAX_K 16
+
+/* cost kinds: ExplicitKernel (core.py:239), ColorKernel (core.py:264), GridKernel (core.py:200) */
+#define LEANOT_COST_STORED 0
+#define LEANOT_COST_POINTS 1
+#define LEANOT_COST_GRID 2
+
+/* Device view of a CostKernel (core.py:167-192).  Normalized entries are
+ * C_ij = mat[(i-row_base)*ld + j] (STORED, already divided by scale) or
+ * raw_ij * inv_scale (POINTS: sum_d |f_id - f_jd|^p; GRID: |drow|^p + |dcol|^p). */
+typedef struct leanot_cost {
+  int32_t kind;
+  int32_t p;          /* exponent 1..3 (POINTS / GRID) */
+  int32_t dim;        /* POINTS feature dimension 1..4 */
+  int32_t height;     /* GRID */
+  int32_t width;      /* GRID */
+  int32_t _pad;
+  int64_t n;          /* number of columns (= global number of rows) */
+  int64_t ld;         /* STORED row stride in doubles (>= n) */
+  int64_t row_base;   /* STORED: global index of the first row held in mat */
+  const double* mat;          /* STORED */
+  const double* feat;         /* POINTS: n x dim row-major */
+  const double* grid_coords;  /* GRID: [row index (n) | column index (n)] as doubles */
+  double inv_scale;   /* 1/scale for on-the-fly kinds */
+  double sup_norm;    /* ||C||_inf after normalization: 1 or 0 */
+} leanot_cost_t;
+
+/* K weight sets {a_k, b_k}: rows softmax_j(-(a_k C_ij + b_kj)) (dxg.py:185-190).
+ * a is a device array of K scalars so CUDA-graph replays see updated values. */
+typedef struct leanot_wsets {
+  int32_t K;
+  int32_t _pad;
+  const double* a;
+  const double* b[LEANOT_MAX_K];
+} leanot_wsets_t;
+
+/* DxgParams (dxg.py:100-128) */
+typedef struct leanot_params {
+  double eta, eta_mu, tau_p, tau_mu, beta, alpha;
+} leanot_params_t;
+
+/* Solver workspace for dxg.solve / dxg_step (dxg.py:261-279, 420-472).  All
+ * pointers are device memory allocated by the caller.  Rows [row0,row1) are
+ * the rows this process sweeps (row sharding across GPUs); column vectors are
+ * full length n.  Sizes: nr = row1-row0, K = 2. */
+typedef struct leanot_dxg_plan {
+  leanot_cost_t cost;
+  leanot_params_t prm;
+  int64_t n, row0, row1;
+  int32_t splits;       /* row splits of the column pass (partial slabs) */
+  int32_t nblk_upd;     /* number of CTAs of the O(n) update kernels */
+  const double* r;      /* n  row marginal */
+  const double* c;      /* n  column marginal */
+  const double* c_tilde;/* n  c + alpha/n */
+  double* delta;        /* n  LogOddsField.delta (state) */
+  double* b;            /* n  TransportLogWeights.b (state) */
+  double* b_bar;        /* n  midpoint weights (derived) */
+  double* bprime;       /* n  scratch (pre-max b) */
+  double* sd;           /* n  2*sup*tanh(delta/2) of the state (dual shift) */
+  double* scal;         /* 8  device scalars: a, a_bar, s, t, sweep count, ... */
+  int64_t* shift;       /* nr row shift (units of ln2/512) for the next sweep */
+  int64_t* m;           /* 2*nr shifts used by the current sweep */
+  double* S;            /* 2*nr row sums */
+  double* coef;         /* 2*nr*4 column-pass polynomial coefficients */
+  double* rowstat;      /* 3*nr  sum e*C, sum e*x, row min (evaluation sweeps) */
+  double* slab;         /* splits*2*n column partials */
+  double* col;          /* 2*n  reduced column marginals (col_now | col_bar) */
+  double* partial;      /* 2*nblk_upd block maxima */
+  double* evalbuf;      /* 16 evaluation scalars */
+  int32_t* flags;       /* 2 + 2*nr fixup list (count, -, entries) */
+} leanot_dxg_plan_t;
+
+/* ---- library ---------------------------------------------------------- */
+int leanot_version(void);
+const char* leanot_last_error(void);
+int leanot_device_sm_count(int device, int* out);
+/* bytes of workspace the sweeps need for given sizes (informational) */
+int leanot_dxg_default_splits(int64_t n, int64_t rows, int* out);
+
+/* ---- cost kernels (core.py:167-288) ----------------------------------- */
+/* rows [i0,i1) of the normalized cost into out (row-major, stride ldo): CostKernel.block */
+int leanot_cost_block(const leanot_cost_t* cost, int64_t i0, int64_t i1, double* out, int64_t ldo, void* stream);
+/* out[0] = max over all entries of the raw matrix (ExplicitKernel scale, core.py:255) */
+int leanot_stored_max(const double* mat, int64_t rows, int64_t cols, int64_t ld, double* out, double* scratch, void* stream);
+/* mat /= scale (in place, IEEE division as core.py:258); also reports min via out_min (negativity check) */
+int leanot_stored_normalize(double* mat, int64_t rows, int64_t cols, int64_t ld, double scale, void* stream);
+/* raw sup over all pairs of ||f_i - f_j||_p^p (ColorKernel scale, core.py:279-284) */
+int leanot_points_sup(const double* feat, int64_t n, int dim, int p, double* out, double* scratch, void* stream);
+/* benchmark instance: C_ij = splitmix64(seed,i,j) -> U[0,1), C[0][n-1] = 1 (oracle/leanot_oracle.py:hash_u01) */
+int leanot_hash_fill(double* mat, int64_t row0, int64_t rows, int64_t n, int64_t ld, uint64_t seed, void* stream);
+
+/* ---- sweeps ------------------------------------------------------------ */
+/* column_marginal for K weight sets (dxg.py:193-208): out[k*n + j] = sum_i r_i softmax_j.
+ * Robust (computes row maxima first); workspace: ws of leanot_sweep_ws_doubles() doubles. */
+int64_t leanot_sweep_ws_doubles(int64_t n, int64_t rows, int K);
+int leanot_column_marginals(const leanot_cost_t* cost, int64_t row0, int64_t row1, const leanot_wsets_t* w,
+                            const double* r, double* out, double* ws, void* stream);
+/* row log-normalizers L[k*nr + i] = LSE_j(-(a_k C_ij + b_kj)) (barycenter.py:78-87, core.py:67-70) */
+int leanot_row_lse(const leanot_cost_t* cost, int64_t row0, int64_t row1, const leanot_wsets_t* w,
+                   double* L, double* ws, void* stream);
+/* _plan_stats (dxg.py:282-310) for one weight set: out3 = {<C,D_r p> (local rows), sum_i r_i H(p_i), -}, col (n) */
+int leanot_plan_stats(const leanot_cost_t* cost, int64_t row0, int64_t row1, const leanot_wsets_t* w,
+                      const double* r, double* col, double* out3, double* ws, void* stream);
+/* row minima min_j (C_ij + v_j) (dxg.py:344-348) */
+int leanot_row_min(const leanot_cost_t* cost, int64_t row0, int64_t row1, const double* v, double* out, void* stream);
+/* exact-max row LSE L_i = LSE_j((sgn*C_ij + v_j)*scale): entropic dual (dxg.py:337), potentials (dxg.py:367),
+ * barycenter dual (barycenter.py:189) */
+int leanot_row_lse_affine(const leanot_cost_t* cost, int64_t row0, int64_t row1, const double* v, double sgn,
+                          double scale, double* L, void* stream);
+
+/* ---- the DXG solver (dxg.py:261-279, 412-472) ------------------------- */
+/* derive b_bar, sd, scalars from the state (call after writing an initial/injected state).
+ * init_shift: 1 = shifts from a=0,b=0 closed form (fresh solve); 0 = compute row maxima. */
+int leanot_dxg_prepare(const leanot_dxg_plan_t* plan, double a, double s, double t, int init_shift, void* stream);
+/* one sweep: both column marginals of the current state into plan->col (local rows).
+ * flags bit0: accumulate evaluation statistics (rowstat, eval sweep). */
+int leanot_dxg_sweep(const leanot_dxg_plan_t* plan, int flags, void* stream);
+/* O(n) updates after plan->col holds the (globally reduced) marginals: state <- next state */
+int leanot_dxg_update(const leanot_dxg_plan_t* plan, void* stream);
+/* evaluation scalars from the last eval sweep: evalbuf[0..] = {cost_rows, ent_rows, inner_rows (eta=0 min
+ * form), infeas, c.d}; eta > 0 additionally runs the LSE dual sweep (dxg.py:335-342). */
+int leanot_dxg_eval(const leanot_dxg_plan_t* plan, void* stream);
+/* iters x (sweep, update) -- capturable; single process only */
+int leanot_dxg_iterate(const leanot_dxg_plan_t* plan, int iters, void* stream);
+/* CUDA graph of `iters` plain iterations (captured once, replayed) */
+int leanot_graph_create(const leanot_dxg_plan_t* plan, int iters, void** graph_exec, void* stream);
+int leanot_graph_launch(void* graph_exec, void* stream);
+int leanot_graph_destroy(void* graph_exec);
+
+/* ---- barycenter (barycenter.py:78-151) --------------------------------- */
+/* r_i proportional to exp(sum_k w_k L_ki), k-sum in sorted order (barycenter.py:90-97) */
+int leanot_bary_rmap(const double* L, int m, int64_t n, const double* w, double* r, double* scratch, void* stream);
+
+/* stream synchronize with error capture */
+int leanot_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEANOT_B200_H */

@@ -1,0 +1,156 @@
+// Shared device code for the DXG sweeps on sm_100a.
+//
+// Numerics: every row softmax of the implicit plan
+//   p_ij = exp(x_ij - L_i),  x_ij = -(a C_ij + b_j)        (dxg.py:199-203)
+// is evaluated with a table-driven FP64 exp whose row shift is an INTEGER in
+// units of ln2/512:  exp(x - m*ln2/512) = 2^((k-m)/512) * exp(r),
+//   k = round(x*512/ln2),  r = x - k*ln2/512,  |r| <= ln2/1024.
+// 2^(j/512) comes from a lane-replicated shared-memory table (conflict-free
+// LDS.64), the 2^e scaling is an integer add on the exponent field, and exp(r)
+// is a degree-3 minimax polynomial (max rel. error 1.1e-15).  Per element and
+// weight set this is 8 FP64 instructions + 6 integer/LDS instructions, versus
+// 16 FP64 for libdevice exp: on sm_100a an FP64 instruction occupies the
+// dispatch port for 2 cycles, so the integer work is not free and is kept
+// minimal (profiles/r01_microbench.md).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/leanot_b200.h"
+
+namespace leanot {
+
+constexpr int LOGN = 9;
+constexpr int NTAB = 1 << LOGN;
+constexpr int TAB_LANES = 16;
+constexpr int TAB_BYTES = NTAB * TAB_LANES * 8;  // 64 KB
+constexpr double LN2 = 0.693147180559945309417232121458;
+constexpr double KINV = 738.6598609351494;        // 512/ln2
+constexpr double LSTEP = 0.0013538128870311432;   // ln2/512
+constexpr double MAGIC = 6755399441055744.0;      // 1.5 * 2^52
+constexpr int KLO = -1000 * NTAB;                 // exp(x-s) < 2^-1000 is flushed to ~2^-1000
+// minimax exp(r) on |r| <= ln2/1024 (relative error <= 1.1e-15), see DESIGN.md §3
+constexpr double EC0 = 0.9999999999999989;
+constexpr double EC1 = 1.0000000000000024;
+constexpr double EC2 = 0.5000000190914873;
+constexpr double EC3 = 0.16666666285067583;
+
+// 2^(j/512), j = 0..511, correctly rounded (filled by the host at library init).
+// The library is one translation unit (leanot_lib.cu includes every .cu file),
+// so this definition exists exactly once.
+__device__ double g_exp2_table[NTAB];
+
+__device__ __forceinline__ void load_table(double* smem_tab) {
+  for (int i = threadIdx.x; i < NTAB * TAB_LANES; i += blockDim.x) smem_tab[i] = g_exp2_table[i >> 4];
+}
+
+// byte offset of this lane's replica inside the table
+__device__ __forceinline__ uint32_t lane_tab_off() { return (threadIdx.x & 15u) << 3; }
+
+// Scaled table value 2^((k - m)/512) for t = fma(x, KINV, MAGIC); the low word of t
+// holds k (mod 2^32), so the subtraction of the row shift is exact modular arithmetic.
+__device__ __forceinline__ double tab_scaled(const char* tab, double t, uint32_t mlo, uint32_t lane_off) {
+  int k = (int)((uint32_t)__double2loint(t) - mlo);
+  k = max(k, KLO);
+  uint32_t off = (((uint32_t)k << 7) & 0xFF80u) | lane_off;
+  double T = *reinterpret_cast<const double*>(tab + off);
+  int hi = __double2hiint(T) + ((k >> LOGN) << 20);
+  return __hiloint2double(hi, __double2loint(T));
+}
+
+// exp(x - m*LSTEP) (pass A form): returns T * poly(r)
+__device__ __forceinline__ double texp(const char* tab, double x, uint32_t mlo, uint32_t lane_off) {
+  double t = fma(x, KINV, MAGIC);
+  double kd = t - MAGIC;
+  double r = fma(kd, -LSTEP, x);
+  double T = tab_scaled(tab, t, mlo, lane_off);
+  double p = fma(fma(EC3, r, EC2), r, EC1);
+  return T * fma(r, p, EC0);
+}
+
+// acc += exp(x - m*LSTEP)
+__device__ __forceinline__ void texp_acc(const char* tab, double x, uint32_t mlo, uint32_t lane_off, double& acc) {
+  double t = fma(x, KINV, MAGIC);
+  double kd = t - MAGIC;
+  double r = fma(kd, -LSTEP, x);
+  double T = tab_scaled(tab, t, mlo, lane_off);
+  double p = fma(fma(EC3, r, EC2), r, EC1);
+  acc = fma(T, fma(r, p, EC0), acc);
+}
+
+// acc += g * exp(x - m*LSTEP) with g folded into the polynomial: gc = g*{EC0..EC3}
+__device__ __forceinline__ void texp_gacc(const char* tab, double x, uint32_t mlo, uint32_t lane_off,
+                                          double g0, double g1, double g2, double g3, double& acc) {
+  double t = fma(x, KINV, MAGIC);
+  double kd = t - MAGIC;
+  double r = fma(kd, -LSTEP, x);
+  double T = tab_scaled(tab, t, mlo, lane_off);
+  double q = fma(fma(fma(g3, r, g2), r, g1), r, g0);
+  acc = fma(T, q, acc);
+}
+
+// ---------------------------------------------------------------------------
+// cost providers (core.py:200-288).  Normalized C_ij = raw_ij * inv_scale for
+// on-the-fly kinds; the stored kind holds the normalized matrix already.
+// ---------------------------------------------------------------------------
+
+struct CostView {
+  int kind, p, dim, height, width;
+  int64_t n, ld, row_base;
+  const double* mat;
+  const double* feat;
+  const double* gcoord;  // grid: [row(n) | col(n)] as doubles
+  double inv_scale;
+};
+
+__host__ __device__ inline CostView make_view(const leanot_cost_t& c) {
+  CostView v;
+  v.kind = c.kind; v.p = c.p; v.dim = c.dim; v.height = c.height; v.width = c.width;
+  v.n = c.n; v.ld = c.ld; v.row_base = c.row_base; v.mat = c.mat; v.feat = c.feat;
+  v.gcoord = c.grid_coords; v.inv_scale = c.inv_scale;
+  return v;
+}
+
+__device__ __forceinline__ double ipow(double d, int p) {
+  d = fabs(d);
+  return p == 1 ? d : (p == 2 ? d * d : d * d * d);
+}
+
+// raw (un-normalized) on-the-fly cost between row features fi and column j
+template <int DIM>
+__device__ __forceinline__ double point_raw(const double* fi, const double* fj, int p) {
+  double s;
+  if (p == 2) {
+    double d0 = fi[0] - fj[0];
+    s = d0 * d0;
+#pragma unroll
+    for (int d = 1; d < DIM; ++d) { double dd = fi[d] - fj[d]; s = fma(dd, dd, s); }
+  } else {
+    s = ipow(fi[0] - fj[0], p);
+#pragma unroll
+    for (int d = 1; d < DIM; ++d) s += ipow(fi[d] - fj[d], p);
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace leanot

@@ -1,0 +1,147 @@
+// Cost providers for the sweeps: one template per CostKernel kind (core.py:200-288).
+// Each provider exposes
+//   Row  row(i)                    per-row data (pointer or coordinates) in registers
+//   Col  col(j)                    per-column data for the column pair (j, j+1)
+//   void eval2(Row, Col, j, c0, c1) normalized C_ij, C_i,j+1
+//   double eval1(Row, j)           single column (tails)
+#pragma once
+#include "leanot_common.cuh"
+
+namespace leanot {
+
+// ExplicitKernel: normalized matrix stored row-major in HBM (core.py:239-261)
+struct CostStored {
+  const double* mat;
+  int64_t ld, row_base;
+  struct Row { const double* p; };
+  struct Col {};
+  __device__ explicit CostStored(const CostView& v) : mat(v.mat), ld(v.ld), row_base(v.row_base) {}
+  __device__ __forceinline__ Row row(int64_t i) const { return Row{mat + (i - row_base) * ld}; }
+  __device__ __forceinline__ Col col(int64_t) const { return Col{}; }
+  __device__ __forceinline__ void eval2(const Row& r, const Col&, int64_t j, double& c0, double& c1) const {
+    double2 v = __ldg(reinterpret_cast<const double2*>(r.p + j));
+    c0 = v.x; c1 = v.y;
+  }
+  // streaming variant for the column pass: evict-first, each row is read once per sweep
+  __device__ __forceinline__ void eval2_stream(const Row& r, const Col&, int64_t j, double& c0, double& c1) const {
+    double2 v = __ldcs(reinterpret_cast<const double2*>(r.p + j));
+    c0 = v.x; c1 = v.y;
+  }
+  __device__ __forceinline__ double eval1(const Row& r, int64_t j) const { return __ldg(r.p + j); }
+};
+
+// ColorKernel: sum_d |f_id - f_jd|^P / scale (core.py:264-288)
+template <int DIM, int P>
+struct CostPoints {
+  const double* f;
+  double inv;
+  int64_t n;
+  struct Row { double v[DIM]; };
+  struct Col { double v0[DIM], v1[DIM]; };
+  __device__ explicit CostPoints(const CostView& v) : f(v.feat), inv(v.inv_scale), n(v.n) {}
+  __device__ __forceinline__ Row row(int64_t i) const {
+    Row r;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) r.v[d] = __ldg(f + i * DIM + d);
+    return r;
+  }
+  __device__ __forceinline__ Col col(int64_t j) const {
+    Col c;
+    int64_t j1 = j + 1 < n ? j + 1 : j;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) { c.v0[d] = __ldg(f + j * DIM + d); c.v1[d] = __ldg(f + j1 * DIM + d); }
+    return c;
+  }
+  __device__ __forceinline__ static double raw(const double* a, const double* b) {
+    double s;
+    if (P == 2) {
+      double d0 = a[0] - b[0];
+      s = d0 * d0;
+#pragma unroll
+      for (int d = 1; d < DIM; ++d) { double dd = a[d] - b[d]; s = fma(dd, dd, s); }
+    } else {
+      double d0 = fabs(a[0] - b[0]);
+      s = P == 1 ? d0 : d0 * d0 * d0;
+#pragma unroll
+      for (int d = 1; d < DIM; ++d) {
+        double dd = fabs(a[d] - b[d]);
+        s += P == 1 ? dd : dd * dd * dd;
+      }
+    }
+    return s;
+  }
+  __device__ __forceinline__ void eval2(const Row& r, const Col& c, int64_t, double& c0, double& c1) const {
+    c0 = raw(r.v, c.v0) * inv;
+    c1 = raw(r.v, c.v1) * inv;
+  }
+  __device__ __forceinline__ void eval2_stream(const Row& r, const Col& c, int64_t j, double& c0, double& c1) const {
+    eval2(r, c, j, c0, c1);
+  }
+  __device__ __forceinline__ double eval1(const Row& r, int64_t j) const {
+    double b[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) b[d] = __ldg(f + j * DIM + d);
+    return raw(r.v, b) * inv;
+  }
+};
+
+// GridKernel: (|drow|^P + |dcol|^P) / scale, cells row-major (core.py:200-236)
+template <int P>
+struct CostGrid {
+  const double* rc;  // [row(n) | col(n)]
+  double inv;
+  int64_t n;
+  struct Row { double r, c; };
+  struct Col { double r0, c0, r1, c1; };
+  __device__ explicit CostGrid(const CostView& v) : rc(v.gcoord), inv(v.inv_scale), n(v.n) {}
+  __device__ __forceinline__ Row row(int64_t i) const { return Row{__ldg(rc + i), __ldg(rc + n + i)}; }
+  __device__ __forceinline__ Col col(int64_t j) const {
+    int64_t j1 = j + 1 < n ? j + 1 : j;
+    return Col{__ldg(rc + j), __ldg(rc + n + j), __ldg(rc + j1), __ldg(rc + n + j1)};
+  }
+  __device__ __forceinline__ static double pw(double d) {
+    d = fabs(d);
+    return P == 1 ? d : (P == 2 ? d * d : d * d * d);
+  }
+  __device__ __forceinline__ void eval2(const Row& r, const Col& c, int64_t, double& c0, double& c1) const {
+    c0 = (pw(r.r - c.r0) + pw(r.c - c.c0)) * inv;
+    c1 = (pw(r.r - c.r1) + pw(r.c - c.c1)) * inv;
+  }
+  __device__ __forceinline__ void eval2_stream(const Row& r, const Col& c, int64_t j, double& c0, double& c1) const {
+    eval2(r, c, j, c0, c1);
+  }
+  __device__ __forceinline__ double eval1(const Row& r, int64_t j) const {
+    return (pw(r.r - __ldg(rc + j)) + pw(r.c - __ldg(rc + n + j))) * inv;
+  }
+};
+
+// Dispatch a functor templated on the provider type for a runtime cost descriptor.
+// F::template run<COST>() must be callable; returns false for unsupported combos.
+#define LEANOT_DISPATCH_COST(view, FN)                                        \
+  [&]() -> int {                                                               \
+    switch ((view).kind) {                                                     \
+      case LEANOT_COST_STORED: return FN.template run<CostStored>();           \
+      case LEANOT_COST_GRID:                                                   \
+        if ((view).p == 1) return FN.template run<CostGrid<1>>();              \
+        if ((view).p == 2) return FN.template run<CostGrid<2>>();              \
+        if ((view).p == 3) return FN.template run<CostGrid<3>>();              \
+        return LEANOT_EINVAL;                                                  \
+      case LEANOT_COST_POINTS:                                                 \
+        if ((view).dim == 1 && (view).p == 1) return FN.template run<CostPoints<1, 1>>(); \
+        if ((view).dim == 1 && (view).p == 2) return FN.template run<CostPoints<1, 2>>(); \
+        if ((view).dim == 1 && (view).p == 3) return FN.template run<CostPoints<1, 3>>(); \
+        if ((view).dim == 2 && (view).p == 1) return FN.template run<CostPoints<2, 1>>(); \
+        if ((view).dim == 2 && (view).p == 2) return FN.template run<CostPoints<2, 2>>(); \
+        if ((view).dim == 2 && (view).p == 3) return FN.template run<CostPoints<2, 3>>(); \
+        if ((view).dim == 3 && (view).p == 1) return FN.template run<CostPoints<3, 1>>(); \
+        if ((view).dim == 3 && (view).p == 2) return FN.template run<CostPoints<3, 2>>(); \
+        if ((view).dim == 3 && (view).p == 3) return FN.template run<CostPoints<3, 3>>(); \
+        if ((view).dim == 4 && (view).p == 1) return FN.template run<CostPoints<4, 1>>(); \
+        if ((view).dim == 4 && (view).p == 2) return FN.template run<CostPoints<4, 2>>(); \
+        if ((view).dim == 4 && (view).p == 3) return FN.template run<CostPoints<4, 3>>(); \
+        return LEANOT_EINVAL;                                                  \
+      default: return LEANOT_EINVAL;                                           \
+    }                                                                          \
+  }()
+
+}  // namespace leanot

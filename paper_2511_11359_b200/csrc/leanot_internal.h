@@ -1,0 +1,55 @@
+// Internal (C++) interfaces between the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/leanot_b200.h"
+#include "leanot_common.cuh"
+
+namespace leanot {
+
+struct RowPassArgs {
+  CostView cost;
+  int64_t i0, i1;              // global rows [i0, i1)
+  const double* a;             // K device scalars
+  const double* b[LEANOT_MAX_K];
+  const int64_t* shift;        // shift[k*shift_kstride + (i-i0)]
+  int64_t shift_kstride;       // 0: one shift per row shared by all weight sets
+  double* S;                   // K x nr row sums
+  int64_t* m_used;             // K x nr shifts used (may be null)
+  // evaluation sweep (weight set 0)
+  double* rowstat;             // 3 x nr: sum e*C, sum e*x, min_j (C_ij + sd_j)
+  const double* sd;
+  // finalize: column-pass coefficients g*EC{0..3}, g = rw_i / S (rw null: g = 1/S)
+  const double* rw;            // indexed by global row
+  double* coef;                // K x nr x 4 (may be null)
+  int64_t* shift_next;         // nr (may be null)
+  int next_from_k;
+  int32_t* flags;              // [count, -, (k, li)...]
+};
+
+struct ColPassArgs {
+  CostView cost;
+  int64_t i0, i1;
+  const double* a;
+  const double* b[LEANOT_MAX_K];
+  const int64_t* m;            // K x nr
+  const double* coef;          // K x nr x 4
+  double* slab;                // splits x K x n
+  int splits;
+};
+
+int num_sms();
+int launch_rowpass(const RowPassArgs& A, int K, bool eval, cudaStream_t st);
+int launch_rowmax(const RowPassArgs& A, int K, int64_t* out, cudaStream_t st);
+int launch_colpass(const ColPassArgs& A, int K, cudaStream_t st);
+int launch_slab_reduce(const double* slab, int splits, int K, int64_t n, double* col, cudaStream_t st);
+int launch_rowlse(const CostView& cv, int64_t i0, int64_t i1, const double* v, double sgn, double scale, double* L,
+                  cudaStream_t st);
+int launch_rowmin(const CostView& cv, int64_t i0, int64_t i1, const double* v, double* out, cudaStream_t st);
+int launch_cost_block(const CostView& cv, int64_t i0, int64_t i1, double* out, int64_t ldo, cudaStream_t st);
+
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+}  // namespace leanot

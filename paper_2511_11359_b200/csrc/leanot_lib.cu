@@ -1,0 +1,4 @@
+// Unity translation unit of libleanot_b200.so (one TU so the exp table symbol
+// and the template instantiations exist exactly once; no -rdc needed).
+#include "leanot_sweep.cu"
+#include "leanot_solver.cu"

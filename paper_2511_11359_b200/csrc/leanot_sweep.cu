@@ -1,0 +1,643 @@
+// n^2 sweeps of the DXG hot path on sm_100a (two-pass form).
+//
+//  pass A (rowpass_kernel): per row i and weight set k
+//      S_ki = sum_j exp(x_kij - m_ki*LSTEP),  x_kij = -(a_k C_ij + b_kj)
+//    with the integer shift m_ki taken from the previous iteration's row
+//    log-normalizer (SURVEY.md §7 hard part 4), so no row-max pass is needed.
+//    Evaluation sweeps also accumulate sum e*C, sum e*x (-> _plan_stats,
+//    dxg.py:282-310) and min_j (C_ij + sd_j) (-> dual_penalized_value at eta=0,
+//    dxg.py:344-348) for weight set 0.
+//  pass B (colpass_kernel): col_kj = sum_i (r_i/S_ki) exp(x_kij - m_ki*LSTEP)
+//    (column_marginal, dxg.py:193-208) for all K weight sets from one read of
+//    each C element; each CTA owns a 512-column tile and a row split and writes a
+//    partial slab; slabs are reduced in fixed order (deterministic, no atomics).
+//
+// Both weight sets of a DXG iteration (current and midpoint weights) are swept
+// together: the midpoint weights depend only on the current state (dxg.py:274).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "leanot_cost.cuh"
+#include "leanot_internal.h"
+
+namespace leanot {
+
+constexpr int RP_THREADS = 256;
+constexpr int CP_THREADS = 256;
+constexpr int CP_TILE = 2 * CP_THREADS;  // columns per column-pass tile
+constexpr int CP_CHUNK = 32;             // rows staged per smem chunk
+
+// S outside [2^-900, 2^900] (or NaN) means the shift was far from the row's
+// log-normalizer: the row is recomputed with an exact max shift (fixup_kernel).
+__device__ __forceinline__ bool sum_ok(double S) { return S >= 0x1p-900 && S <= 0x1p900; }
+
+__device__ __forceinline__ void finalize_row(const RowPassArgs& A, int k, int64_t li, double S, int64_t m) {
+  const int64_t nr = A.i1 - A.i0;
+  A.S[k * nr + li] = S;
+  if (A.m_used) A.m_used[k * nr + li] = m;
+  if (!sum_ok(S)) {
+    int slot = atomicAdd(A.flags, 1);
+    A.flags[2 + 2 * slot] = k;
+    A.flags[3 + 2 * slot] = (int)li;
+    return;
+  }
+  if (A.coef) {
+    double g = A.rw ? A.rw[A.i0 + li] / S : 1.0 / S;
+    double* cf = A.coef + (k * nr + li) * 4;
+    cf[0] = g * EC0; cf[1] = g * EC1; cf[2] = g * EC2; cf[3] = g * EC3;
+  }
+  if (A.shift_next && k == A.next_from_k) A.shift_next[li] = m + llrint(log(S) * (1.0 / LSTEP));
+}
+
+template <class COST, int K, int R, bool EVAL>
+__global__ void __launch_bounds__(RP_THREADS) rowpass_kernel(const RowPassArgs A) {
+  extern __shared__ __align__(16) char smem[];
+  constexpr int NV = R * K + (EVAL ? 3 * R : 0);
+  __shared__ double red[RP_THREADS / 32][NV];
+  load_table(reinterpret_cast<double*>(smem));
+  __syncthreads();
+  const char* tab = smem;
+  const uint32_t loff = lane_tab_off();
+  const COST cost(A.cost);
+  const int64_t n = A.cost.n;
+  const int64_t nr = A.i1 - A.i0;
+  const int64_t nblk = (nr + R - 1) / R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double na[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) na[k] = -A.a[k];
+
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t ib = A.i0 + blk * R;
+    typename COST::Row rows[R];
+    uint32_t mlo[R][K];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      int64_t i = ib + r < A.i1 ? ib + r : A.i1 - 1;
+      rows[r] = cost.row(i);
+#pragma unroll
+      for (int k = 0; k < K; ++k) mlo[r][k] = (uint32_t)A.shift[k * A.shift_kstride + (i - A.i0)];
+    }
+    double acc[R][K];
+    double U[R], V[R], mn[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      U[r] = 0.0; V[r] = 0.0; mn[r] = INFINITY;
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[r][k] = 0.0;
+    }
+    const int64_t nev = n & ~int64_t(1);
+    for (int64_t j = 2 * threadIdx.x; j < nev; j += 2 * RP_THREADS) {
+      const typename COST::Col cl = cost.col(j);
+      double nb0[K], nb1[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double2 bv = __ldg(reinterpret_cast<const double2*>(A.b[k] + j));
+        nb0[k] = -bv.x; nb1[k] = -bv.y;
+      }
+      double2 sdv = make_double2(0.0, 0.0);
+      if (EVAL) sdv = __ldg(reinterpret_cast<const double2*>(A.sd + j));
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double c0, c1;
+        cost.eval2(rows[r], cl, j, c0, c1);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          double x0 = fma(na[k], c0, nb0[k]);
+          double x1 = fma(na[k], c1, nb1[k]);
+          if (EVAL && k == 0) {
+            double e0 = texp(tab, x0, mlo[r][0], loff);
+            double e1 = texp(tab, x1, mlo[r][0], loff);
+            acc[r][0] += e0 + e1;
+            U[r] = fma(e0, c0, fma(e1, c1, U[r]));
+            V[r] = fma(e0, x0, fma(e1, x1, V[r]));
+            mn[r] = fmin(mn[r], fmin(c0 + sdv.x, c1 + sdv.y));
+          } else {
+            texp_acc(tab, x0, mlo[r][k], loff, acc[r][k]);
+            texp_acc(tab, x1, mlo[r][k], loff, acc[r][k]);
+          }
+        }
+      }
+    }
+    if ((n & 1) && threadIdx.x == 0) {  // odd tail column
+      const int64_t j = n - 1;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double c0 = cost.eval1(rows[r], j);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          double x0 = fma(na[k], c0, -__ldg(A.b[k] + j));
+          double e0 = texp(tab, x0, mlo[r][k], loff);
+          acc[r][k] += e0;
+          if (EVAL && k == 0) {
+            U[r] = fma(e0, c0, U[r]);
+            V[r] = fma(e0, x0, V[r]);
+            mn[r] = fmin(mn[r], c0 + __ldg(A.sd + j));
+          }
+        }
+      }
+    }
+    // block reduction in fixed order (deterministic)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double v = warp_sum(acc[r][k]);
+        if (lane == 0) red[warp][r * K + k] = v;
+      }
+      if (EVAL) {
+        double u = warp_sum(U[r]), vv = warp_sum(V[r]), m = warp_min(mn[r]);
+        if (lane == 0) {
+          red[warp][R * K + 3 * r] = u;
+          red[warp][R * K + 3 * r + 1] = vv;
+          red[warp][R * K + 3 * r + 2] = m;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+      const int v = threadIdx.x;
+      const bool is_min = EVAL && v >= R * K && ((v - R * K) % 3 == 2);
+      double t = red[0][v];
+      for (int w = 1; w < RP_THREADS / 32; ++w) t = is_min ? fmin(t, red[w][v]) : t + red[w][v];
+      if (v < R * K) {
+        const int r = v / K, k = v % K;
+        const int64_t i = ib + r;
+        if (i < A.i1) finalize_row(A, k, i - A.i0, t, A.shift[k * A.shift_kstride + (i - A.i0)]);
+      } else if (EVAL) {
+        const int q = v - R * K, r = q / 3, s = q % 3;
+        const int64_t i = ib + r;
+        if (i < A.i1) A.rowstat[s * nr + (i - A.i0)] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Exact recompute of rows whose shifted sum left the safe range (rare: first
+// sweeps of injected states, pathological step sizes).  One CTA, loops the list.
+template <class COST>
+__global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double red[32];
+  __shared__ double bcast;
+  const int cnt = *A.flags;
+  if (cnt == 0) return;
+  load_table(reinterpret_cast<double*>(smem));
+  __syncthreads();
+  const char* tab = smem;
+  const uint32_t loff = lane_tab_off();
+  const COST cost(A.cost);
+  const int64_t n = A.cost.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = 0; e < cnt; ++e) {
+    const int k = A.flags[2 + 2 * e];
+    const int64_t li = A.flags[3 + 2 * e];
+    const int64_t i = A.i0 + li;
+    const typename COST::Row row = cost.row(i);
+    const double na = -A.a[k];
+    double mx = -INFINITY;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = fmax(mx, fma(na, cost.eval1(row, j), -A.b[k][j]));
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < nw; ++w) t = fmax(t, red[w]);
+      bcast = t;
+    }
+    __syncthreads();
+    const int64_t m = llrint(bcast * (1.0 / LSTEP));
+    const uint32_t mlo = (uint32_t)m;
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
+      texp_acc(tab, fma(na, cost.eval1(row, j), -A.b[k][j]), mlo, loff, s);
+    s = warp_sum(s);
+    __syncthreads();
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < nw; ++w) t += red[w];
+      // finalize without re-flagging
+      const int64_t nr = A.i1 - A.i0;
+      A.S[k * nr + li] = t;
+      if (A.m_used) A.m_used[k * nr + li] = m;
+      if (A.coef) {
+        double g = A.rw ? A.rw[i] / t : 1.0 / t;
+        double* cf = A.coef + (k * nr + li) * 4;
+        cf[0] = g * EC0; cf[1] = g * EC1; cf[2] = g * EC2; cf[3] = g * EC3;
+      }
+      if (A.shift_next && k == A.next_from_k) A.shift_next[li] = m + llrint(log(t) * (1.0 / LSTEP));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *A.flags = 0;
+}
+
+// Row maxima of x_kij -> integer shifts (robust start for injected states).
+template <class COST, int K>
+__global__ void __launch_bounds__(RP_THREADS) rowmax_kernel(const RowPassArgs A, int64_t* shift_out) {
+  __shared__ double red[RP_THREADS / 32][K];
+  const COST cost(A.cost);
+  const int64_t n = A.cost.n, nr = A.i1 - A.i0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double na[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) na[k] = -A.a[k];
+  for (int64_t i = A.i0 + blockIdx.x; i < A.i1; i += gridDim.x) {
+    const typename COST::Row row = cost.row(i);
+    double mx[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) mx[k] = -INFINITY;
+    for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) {
+      double c = cost.eval1(row, j);
+#pragma unroll
+      for (int k = 0; k < K; ++k) mx[k] = fmax(mx[k], fma(na[k], c, -__ldg(A.b[k] + j)));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double v = warp_max(mx[k]);
+      if (lane == 0) red[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+      double t = red[0][threadIdx.x];
+      for (int w = 1; w < RP_THREADS / 32; ++w) t = fmax(t, red[w][threadIdx.x]);
+      shift_out[threadIdx.x * nr + (i - A.i0)] = llrint(t * (1.0 / LSTEP));
+    }
+    __syncthreads();
+  }
+}
+
+// pass B: column sums for K weight sets over a row split, written to a slab.
+template <class COST, int K>
+__global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A) {
+  extern __shared__ __align__(16) char smem[];
+  double* s_coef = reinterpret_cast<double*>(smem + TAB_BYTES);       // [CP_CHUNK][K][4]
+  uint32_t* s_m = reinterpret_cast<uint32_t*>(s_coef + CP_CHUNK * K * 4);  // [CP_CHUNK][K]
+  load_table(reinterpret_cast<double*>(smem));
+  __syncthreads();
+  const char* tab = smem;
+  const uint32_t loff = lane_tab_off();
+  const COST cost(A.cost);
+  const int64_t n = A.cost.n, nr = A.i1 - A.i0;
+  const int64_t ntiles = (n + CP_TILE - 1) / CP_TILE;
+  const int64_t items = ntiles * A.splits;
+  const int64_t rows_per_split = (nr + A.splits - 1) / A.splits;
+  double na[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) na[k] = -A.a[k];
+
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t tile = it % ntiles, split = it / ntiles;
+    const int64_t j = tile * CP_TILE + 2 * threadIdx.x;
+    const bool v0 = j < n, v1 = j + 1 < n;
+    const typename COST::Col cl = cost.col(v1 ? j : (v0 ? j : 0));
+    double nb0[K], nb1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      nb0[k] = v0 ? -__ldg(A.b[k] + j) : 0.0;
+      nb1[k] = v1 ? -__ldg(A.b[k] + j + 1) : 0.0;
+    }
+    double acc0[K], acc1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { acc0[k] = 0.0; acc1[k] = 0.0; }
+    const int64_t rs0 = A.i0 + split * rows_per_split;
+    const int64_t rs1 = A.i1 < rs0 + rows_per_split ? A.i1 : rs0 + rows_per_split;
+    for (int64_t q0 = rs0; q0 < rs1; q0 += CP_CHUNK) {
+      const int nq = (int)(rs1 - q0 < CP_CHUNK ? rs1 - q0 : CP_CHUNK);
+      __syncthreads();
+      for (int t = threadIdx.x; t < nq * K * 4; t += CP_THREADS) {
+        int q = t / (K * 4), k = (t / 4) % K, c = t % 4;
+        s_coef[t] = A.coef[(k * nr + (q0 - A.i0 + q)) * 4 + c];
+      }
+      for (int t = threadIdx.x; t < nq * K; t += CP_THREADS) {
+        int q = t / K, k = t % K;
+        s_m[t] = (uint32_t)A.m[k * nr + (q0 - A.i0 + q)];
+      }
+      __syncthreads();
+      if (v0) {
+#pragma unroll 2
+        for (int q = 0; q < nq; ++q) {
+          const typename COST::Row row = cost.row(q0 + q);
+          double c0, c1;
+          if (v1) {
+            cost.eval2_stream(row, cl, j, c0, c1);
+          } else {
+            c0 = cost.eval1(row, j);
+            c1 = c0;
+          }
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const double* cf = s_coef + (q * K + k) * 4;
+            const double g0 = cf[0], g1 = cf[1], g2 = cf[2], g3 = cf[3];
+            const uint32_t mlo = s_m[q * K + k];
+            texp_gacc(tab, fma(na[k], c0, nb0[k]), mlo, loff, g0, g1, g2, g3, acc0[k]);
+            texp_gacc(tab, fma(na[k], c1, nb1[k]), mlo, loff, g0, g1, g2, g3, acc1[k]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double* out = A.slab + (split * K + k) * n;
+      if (v0) out[j] = acc0[k];
+      if (v1) out[j + 1] = acc1[k];
+    }
+  }
+}
+
+// col[k][j] = sum over splits in fixed order
+__global__ void slab_reduce_kernel(const double* __restrict__ slab, int splits, int K, int64_t n, double* __restrict__ col) {
+  const int64_t total = (int64_t)K * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < splits; ++q) s += slab[q * total + t];
+    col[t] = s;
+  }
+}
+
+// Row LSE with exact max, for the entropic dual / potentials / barycenter dual:
+//   L_i = LSE_j( (sgn * C_ij + v_j) * scale )   (dxg.py:337, 367; barycenter.py:189)
+// two reads of the row (max, then shifted sum); evaluation-only.
+template <class COST>
+__global__ void __launch_bounds__(RP_THREADS) rowlse_kernel(const CostView cv, int64_t i0, int64_t i1, const double* v,
+                                                           double sgn, double scale, double* L) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double red[RP_THREADS / 32];
+  __shared__ double bc;
+  load_table(reinterpret_cast<double*>(smem));
+  __syncthreads();
+  const char* tab = smem;
+  const uint32_t loff = lane_tab_off();
+  const COST cost(cv);
+  const int64_t n = cv.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
+    const typename COST::Row row = cost.row(i);
+    double mx = -INFINITY;
+    for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) mx = fmax(mx, (sgn * cost.eval1(row, j) + __ldg(v + j)) * scale);
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < RP_THREADS / 32; ++w) t = fmax(t, red[w]);
+      bc = t;
+    }
+    __syncthreads();
+    const double xm = bc;
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) {
+      double y = (sgn * cost.eval1(row, j) + __ldg(v + j)) * scale - xm;
+      texp_acc(tab, fmax(y, -1000.0), 0u, loff, s);
+    }
+    s = warp_sum(s);
+    __syncthreads();
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < RP_THREADS / 32; ++w) t += red[w];
+      L[i - i0] = xm + log(t);
+    }
+    __syncthreads();
+  }
+}
+
+// min_j (C_ij + v_j) per row (dxg.py:344-348)
+template <class COST>
+__global__ void __launch_bounds__(RP_THREADS) rowmin_kernel(const CostView cv, int64_t i0, int64_t i1, const double* v, double* out) {
+  __shared__ double red[RP_THREADS / 32];
+  const COST cost(cv);
+  const int64_t n = cv.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
+    const typename COST::Row row = cost.row(i);
+    double mn = INFINITY;
+    for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) mn = fmin(mn, cost.eval1(row, j) + __ldg(v + j));
+    mn = warp_min(mn);
+    if (lane == 0) red[warp] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < RP_THREADS / 32; ++w) t = fmin(t, red[w]);
+      out[i - i0] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// CostKernel.block: rows [i0,i1) of the normalized cost
+template <class COST>
+__global__ void cost_block_kernel(const CostView cv, int64_t i0, int64_t i1, double* out, int64_t ldo) {
+  const COST cost(cv);
+  const int64_t n = cv.n;
+  for (int64_t i = i0 + blockIdx.y; i < i1; i += gridDim.y) {
+    const typename COST::Row row = cost.row(i);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+      out[(i - i0) * ldo + j] = cost.eval1(row, j);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+
+int g_num_sms = 0;
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <class COST, int K, int R, bool EVAL>
+static int launch_rowpass_t(const RowPassArgs& A, cudaStream_t st) {
+  auto kern = rowpass_kernel<COST, K, R, EVAL>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess) return LEANOT_ECUDA;
+    attr = true;
+  }
+  const int64_t nr = A.i1 - A.i0;
+  const int64_t nblk = (nr + R - 1) / R;
+  int grid = (int)std::min<int64_t>(nblk, (int64_t)num_sms() * 3);
+  if (grid < 1) return LEANOT_OK;
+  kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(A);
+  return LEANOT_OK;
+}
+
+template <class COST>
+static int launch_fixup_t(const RowPassArgs& A, cudaStream_t st) {
+  auto kern = fixup_kernel<COST>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess) return LEANOT_ECUDA;
+    attr = true;
+  }
+  kern<<<1, 1024, TAB_BYTES, st>>>(A);
+  return LEANOT_OK;
+}
+
+struct RowPassFn {
+  const RowPassArgs& A;
+  int K;
+  bool eval;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    int rc;
+    if (K == 1) rc = eval ? launch_rowpass_t<COST, 1, 4, true>(A, st) : launch_rowpass_t<COST, 1, 4, false>(A, st);
+    else if (K == 2) rc = eval ? launch_rowpass_t<COST, 2, 4, true>(A, st) : launch_rowpass_t<COST, 2, 4, false>(A, st);
+    else return LEANOT_EINVAL;
+    if (rc != LEANOT_OK) return rc;
+    if (A.flags) return launch_fixup_t<COST>(A, st);
+    return LEANOT_OK;
+  }
+};
+
+int launch_rowpass(const RowPassArgs& A, int K, bool eval, cudaStream_t st) {
+  RowPassFn f{A, K, eval, st};
+  return LEANOT_DISPATCH_COST(A.cost, f);
+}
+
+struct RowMaxFn {
+  const RowPassArgs& A;
+  int K;
+  int64_t* out;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    const int64_t nr = A.i1 - A.i0;
+    int grid = (int)std::min<int64_t>(nr, (int64_t)num_sms() * 8);
+    if (grid < 1) return LEANOT_OK;
+    if (K == 1) rowmax_kernel<COST, 1><<<grid, RP_THREADS, 0, st>>>(A, out);
+    else if (K == 2) rowmax_kernel<COST, 2><<<grid, RP_THREADS, 0, st>>>(A, out);
+    else return LEANOT_EINVAL;
+    return LEANOT_OK;
+  }
+};
+
+int launch_rowmax(const RowPassArgs& A, int K, int64_t* out, cudaStream_t st) {
+  RowMaxFn f{A, K, out, st};
+  return LEANOT_DISPATCH_COST(A.cost, f);
+}
+
+template <class COST, int K>
+static int launch_colpass_t(const ColPassArgs& A, cudaStream_t st) {
+  auto kern = colpass_kernel<COST, K>;
+  const int smem = TAB_BYTES + CP_CHUNK * K * 4 * 8 + CP_CHUNK * K * 4;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return LEANOT_ECUDA;
+    attr = true;
+  }
+  const int64_t n = A.cost.n;
+  const int64_t items = ((n + CP_TILE - 1) / CP_TILE) * A.splits;
+  int grid = (int)std::min<int64_t>(items, (int64_t)num_sms() * 3);
+  if (grid < 1) return LEANOT_OK;
+  kern<<<grid, CP_THREADS, smem, st>>>(A);
+  return LEANOT_OK;
+}
+
+struct ColPassFn {
+  const ColPassArgs& A;
+  int K;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    if (K == 1) return launch_colpass_t<COST, 1>(A, st);
+    if (K == 2) return launch_colpass_t<COST, 2>(A, st);
+    return LEANOT_EINVAL;
+  }
+};
+
+int launch_colpass(const ColPassArgs& A, int K, cudaStream_t st) {
+  ColPassFn f{A, K, st};
+  return LEANOT_DISPATCH_COST(A.cost, f);
+}
+
+int launch_slab_reduce(const double* slab, int splits, int K, int64_t n, double* col, cudaStream_t st) {
+  const int64_t total = (int64_t)K * n;
+  int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 4);
+  if (grid < 1) return LEANOT_OK;
+  slab_reduce_kernel<<<grid, 256, 0, st>>>(slab, splits, K, n, col);
+  return LEANOT_OK;
+}
+
+struct RowLseFn {
+  const CostView& cv;
+  int64_t i0, i1;
+  const double* v;
+  double sgn, scale;
+  double* L;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    auto kern = rowlse_kernel<COST>;
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess) return LEANOT_ECUDA;
+      attr = true;
+    }
+    int grid = (int)std::min<int64_t>(i1 - i0, (int64_t)num_sms() * 3);
+    if (grid < 1) return LEANOT_OK;
+    kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(cv, i0, i1, v, sgn, scale, L);
+    return LEANOT_OK;
+  }
+};
+
+int launch_rowlse(const CostView& cv, int64_t i0, int64_t i1, const double* v, double sgn, double scale, double* L,
+                  cudaStream_t st) {
+  RowLseFn f{cv, i0, i1, v, sgn, scale, L, st};
+  return LEANOT_DISPATCH_COST(cv, f);
+}
+
+struct RowMinFn {
+  const CostView& cv;
+  int64_t i0, i1;
+  const double* v;
+  double* out;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    int grid = (int)std::min<int64_t>(i1 - i0, (int64_t)num_sms() * 8);
+    if (grid < 1) return LEANOT_OK;
+    rowmin_kernel<COST><<<grid, RP_THREADS, 0, st>>>(cv, i0, i1, v, out);
+    return LEANOT_OK;
+  }
+};
+
+int launch_rowmin(const CostView& cv, int64_t i0, int64_t i1, const double* v, double* out, cudaStream_t st) {
+  RowMinFn f{cv, i0, i1, v, out, st};
+  return LEANOT_DISPATCH_COST(cv, f);
+}
+
+struct CostBlockFn {
+  const CostView& cv;
+  int64_t i0, i1;
+  double* out;
+  int64_t ldo;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    dim3 grid((unsigned)std::min<int64_t>((cv.n + 255) / 256, 64), (unsigned)std::min<int64_t>(i1 - i0, 4096));
+    if (i1 <= i0) return LEANOT_OK;
+    cost_block_kernel<COST><<<grid, 256, 0, st>>>(cv, i0, i1, out, ldo);
+    return LEANOT_OK;
+  }
+};
+
+int launch_cost_block(const CostView& cv, int64_t i0, int64_t i1, double* out, int64_t ldo, cudaStream_t st) {
+  CostBlockFn f{cv, i0, i1, out, ldo, st};
+  return LEANOT_DISPATCH_COST(cv, f);
+}
+
+}  // namespace leanot

@@ -1,0 +1,221 @@
+"""Device engine of the DXG solver: buffers in HBM, launches through the C ABI.
+
+One `DxgEngine` owns the O(n) state of one solve (dual log-odds delta, plan
+log-weights b, scalars a/s/t on device) plus the sweep workspaces, and runs:
+
+    sweep   both column marginals of the current state (pass A + pass B)
+            [+ NCCL combine of the column partials when rows are sharded]
+    update  the fused O(n) updates of dxg_step (dxg.py:273-278)
+    eval    the _evaluate scalars (dxg.py:412-417) from the last eval sweep
+
+Rows can be sharded over a torch.distributed group (one process per GPU):
+each rank sweeps rows [row0, row1) of C; the only exchange per iteration is the
+2n-vector of column partials (all-gather, summed in rank order so the result is
+deterministic), plus 3 scalars on evaluation iterations.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DxgEngine:
+    def __init__(self, kernel, r, c, params, group=None, device=None, splits=None):
+        torch = _torch()
+        self.kernel = kernel
+        self.device = kernel.device if device is None else torch.device(device)
+        self.n = n = kernel.n
+        self.group = group
+        self.world = 1
+        self.rank = 0
+        if group is not None:
+            import torch.distributed as dist
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        r0, r1 = kernel.local_rows
+        if self.world > 1 and (r0, r1) == (0, n):
+            per = (n + self.world - 1) // self.world
+            r0, r1 = min(n, self.rank * per), min(n, (self.rank + 1) * per)
+        if r1 <= r0:
+            raise ValueError("empty row shard")
+        self.row0, self.row1 = r0, r1
+        nr = r1 - r0
+        L = _lib.lib()
+        if splits is None:
+            s = C.c_int(1)
+            L.leanot_dxg_default_splits(n, nr, C.byref(s))
+            splits = s.value
+        nblk = int(min(max(1, (n + 255) // 256), 2 * self._sms()))
+        dev = self.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        rw = np.asarray(r, dtype=float)
+        cw = np.asarray(c, dtype=float)
+        self.r = torch.from_numpy(rw).to(dev)
+        self.c = torch.from_numpy(cw).to(dev)
+        self.c_tilde = self.c + params.alpha / n  # c.weights + alpha/n (dxg.py:269)
+        self.delta = torch.zeros(n, **f64)
+        self.b = torch.zeros(n, **f64)
+        self.b_bar = torch.zeros(n, **f64)
+        self.bprime = torch.zeros(n, **f64)
+        self.sd = torch.zeros(n, **f64)
+        self.scal = torch.zeros(8, **f64)
+        self.shift = torch.zeros(nr, dtype=torch.int64, device=dev)
+        self.m = torch.zeros(2 * nr, dtype=torch.int64, device=dev)
+        self.S = torch.zeros(2 * nr, **f64)
+        self.coef = torch.zeros(8 * nr, **f64)
+        self.rowstat = torch.zeros(3 * nr, **f64)
+        self.slab = torch.zeros(splits * 2 * n, **f64)
+        self.col = torch.zeros(2 * n, **f64)
+        self.partial = torch.zeros(2 * nblk, **f64)
+        self.evalbuf = torch.zeros(16, **f64)
+        self.flags = torch.zeros(2 + 4 * nr, dtype=torch.int32, device=dev)
+        self.params = params
+        self.plan = _lib.DxgPlanT()
+        p = self.plan
+        p.cost = kernel.cost_struct()
+        p.prm = _lib.ParamsT(params.eta, params.eta_mu, params.tau_p, params.tau_mu, params.beta, params.alpha)
+        p.n, p.row0, p.row1, p.splits, p.nblk_upd = n, r0, r1, int(splits), nblk
+        for name in ("r", "c", "c_tilde", "delta", "b", "b_bar", "bprime", "sd", "scal", "shift", "m", "S",
+                     "coef", "rowstat", "slab", "col", "partial", "evalbuf", "flags"):
+            setattr(p, name, getattr(self, name).data_ptr())
+        self._graphs = {}
+        pos = rw > 0
+        self.h_r = float(-(rw[pos] * np.log(rw[pos])).sum())  # H(r) (dxg.py:308-309, 340-341)
+        if self.world > 1:
+            self._gather = torch.empty((self.world, 2 * n), **f64)
+
+    def _sms(self):
+        v = C.c_int(148)
+        _lib.lib().leanot_device_sm_count(self.device.index or 0, C.byref(v))
+        return v.value
+
+    # -- state ------------------------------------------------------------------
+    def load_state(self, delta, b, a, s, t, fresh=False):
+        torch = _torch()
+        self.delta.copy_(torch.as_tensor(np.asarray(delta, dtype=float)))
+        self.b.copy_(torch.as_tensor(np.asarray(b, dtype=float)))
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().leanot_dxg_prepare(C.byref(self.plan), float(a), float(s), float(t),
+                                                     1 if fresh else 0, _lib.stream_handle()), "dxg_prepare")
+
+    def read_state(self):
+        sc = self.scal[:4].cpu().tolist()
+        return self.delta.cpu().numpy(), self.b.cpu().numpy(), sc[0], sc[2], int(round(sc[3]))
+
+    def scalars(self):
+        return self.scal[:4].cpu().tolist()
+
+    # -- iteration ---------------------------------------------------------------
+    def _stream(self):
+        return _lib.stream_handle()
+
+    def sweep(self, evaluate=False):
+        with _torch().cuda.device(self.device):
+            _lib.check(_lib.lib().leanot_dxg_sweep(C.byref(self.plan), 1 if evaluate else 0, self._stream()),
+                       "dxg_sweep")
+        if self.world > 1:
+            self._combine_cols()
+
+    def _combine_cols(self):
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(self._gather, self.col, group=self.group)
+        # fixed rank order -> identical result on every rank
+        acc = self._gather[0].clone()
+        for q in range(1, self.world):
+            acc += self._gather[q]
+        self.col.copy_(acc)
+
+    def update(self):
+        with _torch().cuda.device(self.device):
+            _lib.check(_lib.lib().leanot_dxg_update(C.byref(self.plan), self._stream()), "dxg_update")
+
+    def iterate(self, iters: int, use_graph: bool | None = None):
+        """iters x (sweep, update) with no evaluation."""
+        if iters <= 0:
+            return
+        if self.world > 1:
+            for _ in range(iters):
+                self.sweep()
+                self.update()
+            return
+        L = _lib.lib()
+        if use_graph is None:
+            use_graph = self.n <= 20000
+        with _torch().cuda.device(self.device):
+            if not use_graph:
+                _lib.check(L.leanot_dxg_iterate(C.byref(self.plan), int(iters), self._stream()), "dxg_iterate")
+                return
+            g = self._graphs.get(iters)
+            if g is None:
+                h = C.c_void_p()
+                _lib.check(L.leanot_graph_create(C.byref(self.plan), int(iters), C.byref(h), self._stream()),
+                           "graph_create")
+                g = self._graphs[iters] = h
+            _lib.check(L.leanot_graph_launch(g, self._stream()), "graph_launch")
+
+    def evaluate(self):
+        """(primal, dual, infeas, s) of the state swept by the last sweep(evaluate=True)."""
+        torch = _torch()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().leanot_dxg_eval(C.byref(self.plan), self._stream()), "dxg_eval")
+        buf = self.evalbuf[:5]
+        if self.world > 1:
+            import torch.distributed as dist
+            rows = buf[:3].clone()
+            gathered = torch.empty((self.world, 3), dtype=torch.float64, device=self.device)
+            dist.all_gather_into_tensor(gathered, rows, group=self.group)
+            vals = gathered.cpu().numpy()
+            cost_v, ent_rows, inner_rows = (float(sum(vals[q, k] for q in range(self.world))) for k in range(3))
+            infeas, cd = buf[3:5].cpu().tolist()
+        else:
+            cost_v, ent_rows, inner_rows, infeas, cd = buf.cpu().tolist()
+        eta = self.params.eta
+        sup = self.kernel.sup_norm
+        ent = ent_rows + self.h_r
+        primal = cost_v + 2.0 * sup * infeas - eta * ent            # dxg.py:415
+        if eta > 0:
+            inner = -eta * inner_rows - eta * self.h_r                # dxg.py:342
+        else:
+            inner = inner_rows                                       # dxg.py:348
+        dual = float(-2.0 * sup * cd + inner)                        # dxg.py:349
+        return primal, dual, infeas
+
+    def col_now(self):
+        return self.col[: self.n].cpu().numpy()
+
+    def close(self):
+        L = _lib.lib()
+        for g in self._graphs.values():
+            L.leanot_graph_destroy(g)
+        self._graphs.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def default_group():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            return dist.group.WORLD
+    except Exception:
+        pass
+    return None
+
+
+def check_finite(x, what):
+    if not math.isfinite(x):
+        raise RuntimeError(f"non-finite {what}")

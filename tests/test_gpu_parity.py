@@ -1,0 +1,185 @@
+"""CUDA path vs the reference's golden vectors and the oracle (needs a B200).
+
+Tolerances (north_star): duals and marginals within 1e-10 relative per
+iteration; final transport cost within 1e-8 relative; same iteration count to
+eps.  Relative errors are norm-wise (max |x - ref| / max |ref|).
+"""
+
+import numpy as np
+import pytest
+
+import leanot_oracle as O
+from helpers import device_cost, golden_names, load, oracle_cost, params_from, rel_err
+
+pytestmark = pytest.mark.gpu
+
+SWEEPS = golden_names("sweep_")
+STEPS = golden_names("step_")
+SOLVES = golden_names("solve_")
+TOL_ITER = 1e-10
+
+
+def _dxg():
+    from paper_2511_11359_b200 import dxg
+    return dxg
+
+
+@pytest.mark.parametrize("name", SWEEPS)
+def test_column_marginal_vs_reference(name):
+    dxg = _dxg()
+    d = load(name)
+    k = device_cost(d)
+    for t in range(3):
+        w = dxg.TransportLogWeights(float(d[f"case{t}_a"]), d[f"case{t}_b"], 0.0, 0)
+        col = dxg.column_marginal(w, k, d["r"])
+        assert rel_err(col, d[f"case{t}_col"]) <= 1e-13, t
+        assert abs(col.sum() - 1.0) <= 1e-12
+
+
+@pytest.mark.parametrize("name", SWEEPS)
+def test_evaluation_functions_vs_reference(name):
+    dxg = _dxg()
+    d = load(name)
+    k = device_cost(d)
+    r, c = d["r"], d["c"]
+    for t in range(3):
+        w = dxg.TransportLogWeights(float(d[f"case{t}_a"]), d[f"case{t}_b"], 0.0, 0)
+        mu = dxg.LogOddsField(d[f"case{t}_delta"])
+        cost, col, ent = dxg._plan_stats(w, k, r)
+        assert abs(cost - float(d[f"case{t}_cost"])) <= 1e-13 * max(1, abs(cost))
+        assert abs(ent - float(d[f"case{t}_ent"])) <= 1e-12 * max(1, abs(ent))
+        assert abs(dxg.primal_penalized_value(w, k, r, c, 0.0) - float(d[f"case{t}_prim0"])) <= 1e-12
+        assert abs(dxg.primal_penalized_value(w, k, r, c, 1e-3) - float(d[f"case{t}_prim3"])) <= 1e-12
+        assert abs(dxg.dual_penalized_value(mu, k, r, c, 0.0) - float(d[f"case{t}_dual0"])) <= 1e-13
+        assert abs(dxg.dual_penalized_value(mu, k, r, c, 1e-3) - float(d[f"case{t}_dual3"])) <= 1e-12
+        assert abs(dxg.dual_penalized_value(mu, k, r, c, 1e-7) - float(d[f"case{t}_dual7"])) <= 1e-12
+    pot = dxg.recover_eot_potentials(dxg.DxgState.initial(k.n), dxg.LogOddsField(d["case1_delta"]), k,
+                                     d["r_full"], 1e-2)
+    assert rel_err(pot.phi, d["pot_phi"]) <= 1e-11
+    assert rel_err(pot.psi, d["pot_psi"]) <= 1e-14
+
+
+SCHEMES = ["tuned", "tuned_taumu005", "tuned_eta1e-3", "loose", "li"]
+
+
+@pytest.mark.parametrize("name", STEPS)
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_dxg_step_injected_state(name, scheme):
+    """Single-step parity from injected states: valid in every regime, chaotic ones included."""
+    dxg = _dxg()
+    d = load(name)
+    k = device_cost(d)
+    prm = dxg.DxgParams(*[float(v) for v in d[f"{scheme}_params"]])
+    a, s, t = d[f"{scheme}_in_scalars"]
+    st = dxg.DxgState(dxg.LogOddsField(d[f"{scheme}_in_delta"]),
+                      dxg.TransportLogWeights(float(a), d[f"{scheme}_in_b"], float(s), int(t)))
+    nxt = dxg.dxg_step(st, k, d["r"], d["c"], prm)
+    assert rel_err(nxt.mu.delta, d[f"{scheme}_out_delta"]) <= TOL_ITER
+    assert rel_err(nxt.weights.b, d[f"{scheme}_out_b"]) <= TOL_ITER
+    assert [nxt.weights.a, nxt.weights.s, nxt.weights.t] == d[f"{scheme}_out_scalars"].tolist()
+
+
+@pytest.mark.parametrize("name", STEPS)
+@pytest.mark.parametrize("scheme", ["tuned_taumu005", "loose", "li", "tuned_eta1e-3"])
+def test_trajectory_per_iteration(name, scheme):
+    """40 iterations from the zero state through the solver engine, every iterate within 1e-10."""
+    from paper_2511_11359_b200.engine import DxgEngine
+    d = load(name)
+    k = device_cost(d)
+    dxg = _dxg()
+    prm = dxg.DxgParams(*[float(v) for v in d[f"{scheme}_params"]])
+    eng = DxgEngine(k, d["r"], d["c"], prm)
+    n = k.n
+    eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
+    for it in range(d[f"{scheme}_traj_delta"].shape[0]):
+        eng.sweep()
+        eng.update()
+        delta, b, a, s, t = eng.read_state()
+        assert rel_err(delta, d[f"{scheme}_traj_delta"][it]) <= TOL_ITER, it
+        assert rel_err(b, d[f"{scheme}_traj_b"][it]) <= TOL_ITER, it
+    assert [a, s, t] == d[f"{scheme}_traj_scalars"].tolist()
+
+
+@pytest.mark.parametrize("name", SOLVES)
+def test_solve_vs_reference(name):
+    """Same iteration count, same converged flag, trajectory and final cost."""
+    dxg = _dxg()
+    d = load(name)
+    k = device_cost(d)
+    prm = dxg.DxgParams(*[float(v) for v in d["params"]])
+    term = dxg.Termination(eps=float(d["term"][0]), max_iter=int(d["term"][1]))
+    sol = dxg.solve(k, d["r"], d["c"], prm, term, log_stride=25, dense_cap=0)
+    assert sol.iterations == int(d["iterations"])
+    assert sol.converged == bool(d["converged"])
+    got = np.array([[p.iter, p.primal, p.dual, p.gap, p.col_infeas_l1, p.s] for p in sol.trajectory])
+    ref = d["traj"]
+    assert got.shape == ref.shape and np.array_equal(got[:, 0], ref[:, 0])
+    if "tuned_maxiter" not in name:
+        assert rel_err(got[:, 1], ref[:, 1]) <= 1e-8       # primal (transport cost)
+        assert rel_err(got[:, 2], ref[:, 2]) <= 1e-8
+        assert rel_err(sol.state.mu.delta, d["delta"]) <= 1e-8
+    assert abs(sol.report.col_gap - float(d["col_gap"])) <= 1e-8 * max(1.0, float(d["col_gap"])) + 1e-14
+
+
+def test_hash_kernel_matches_oracle_bits():
+    from paper_2511_11359_b200 import core
+    hk = core.HashKernel(1001, seed=3)
+    hc = O.HashCost(1001, seed=3)
+    for i0, i1 in ((0, 5), (500, 503), (998, 1001)):
+        assert np.array_equal(hk.block(i0, i1), hc.block(i0, i1))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 513, 1000])
+def test_random_sizes_vs_oracle(n):
+    """Ragged sizes (odd n, partial tiles) against the oracle."""
+    dxg = _dxg()
+    from paper_2511_11359_b200 import core
+    rng = np.random.default_rng(n)
+    Cm = rng.random((n, n)) * 5
+    r = O.normalized_hist(rng.random(n))
+    c = O.normalized_hist(rng.random(n))
+    k = core.ExplicitKernel(Cm)
+    ok = O.DenseCost(Cm)
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    st = dxg.DxgState(dxg.LogOddsField(rng.uniform(-1, 1, n)),
+                      dxg.TransportLogWeights(40.0, -np.abs(rng.normal(0, 20, n)), 0.0, 40))
+    nxt = dxg.dxg_step(st, k, r, c, prm)
+    onxt = O.step(O.Iterate(st.mu.delta, 40.0, st.weights.b, 0.0, 40), ok, r, c,
+                  O.params_tuned(0.0, tau_mu=0.05))
+    assert rel_err(nxt.mu.delta, onxt.delta) <= TOL_ITER
+    assert rel_err(nxt.weights.b, onxt.b) <= TOL_ITER
+
+
+def test_zero_cost_and_sparse_marginal():
+    """C == 0 (sup_norm 0) and r with zeros: the SPEC fixed point."""
+    dxg = _dxg()
+    from paper_2511_11359_b200 import core
+    n = 40
+    k = core.ExplicitKernel(np.zeros((n, n)))
+    assert k.sup_norm == 0.0 and k.scale == 1.0
+    r = np.zeros(n)
+    r[:10] = 0.1
+    c = np.full(n, 1.0 / n)
+    prm = dxg.params_tuned(0.0)
+    st = dxg.DxgState.initial(n)
+    for _ in range(3):
+        st = dxg.dxg_step(st, k, r, c, prm)
+    assert np.allclose(st.mu.delta, 0.0, atol=1e-14)
+    col = dxg.column_marginal(st.weights, k, r)
+    assert np.allclose(col, 1.0 / n, atol=1e-15)
+
+
+def test_large_dynamic_range_shift_fixup():
+    """Injected state far from any previous shift: rows must be recomputed exactly."""
+    dxg = _dxg()
+    from paper_2511_11359_b200 import core
+    n = 300
+    rng = np.random.default_rng(5)
+    Cm = rng.random((n, n))
+    k = core.ExplicitKernel(Cm)
+    r = O.normalized_hist(rng.random(n))
+    for a, bscale in ((3000.0, 1500.0), (1e5, 10.0), (0.0, 900.0)):
+        b = -np.abs(rng.normal(0, bscale, n))
+        col = dxg.column_marginal(dxg.TransportLogWeights(a, b, 0.0, 0), k, r)
+        (ref,) = O.column_marginals(O.DenseCost(Cm), r, [(a, b)])
+        assert rel_err(col, ref) <= 1e-11

@@ -1,0 +1,92 @@
+"""Host-side logic that needs no GPU: parameter schemes, validation, error behaviour."""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2511_11359_b200 import dxg
+from paper_2511_11359_b200.core import Histogram
+from paper_2511_11359_b200.rounding import DenseCoupling, infeasibility
+
+
+def test_params_tuned_matches_spec():
+    p = dxg.params_tuned(0.0)
+    assert (p.tau_p, p.tau_mu, p.beta, p.alpha, p.eta_mu, p.eta) == (1.0, 1.0, 1.1, 0.01, 0.0, 0.0)
+
+
+def test_params_li_spec_example():
+    p = dxg.params_li(1024, 0.01)
+    assert abs(p.beta - 1153.66) < 0.01
+    assert abs(p.tau_p - 0.02944) < 1e-5
+    assert abs(p.tau_mu - 509.5) < 0.1
+    assert abs(p.tau_p * p.tau_mu - 15.0) < 1e-12
+
+
+def test_params_loose_spec_example():
+    p = dxg.params_loose(1024, 0.01, 1e-3)   # SPEC.md:270 (reference computes 9.0168e-5)
+    assert abs(p.eta - 0.01 / (16 * math.log(1024))) < 1e-18
+    assert p.tau_mu == 1.0 / 128 and p.beta == math.log(3.0)
+    assert p.tau_mu * p.eta_mu <= p.tau_p * p.eta + 1e-18
+
+
+@pytest.mark.parametrize("kw", [dict(eta=-1.0), dict(tau_p=0.0), dict(beta=0.0), dict(alpha=2.0),
+                                dict(eta=2.0, tau_p=1.0)])
+def test_params_validation(kw):
+    base = dict(eta=0.0, eta_mu=0.0, tau_p=1.0, tau_mu=1.0, beta=1.1, alpha=0.01)
+    base.update(kw)
+    with pytest.raises(ValueError):
+        dxg.DxgParams(**base)
+
+
+def test_histogram_validation():
+    with pytest.raises(ValueError):
+        Histogram(np.array([]))
+    with pytest.raises(ValueError):
+        Histogram(np.array([0.5, -0.1, 0.6]))
+    with pytest.raises(ValueError):
+        Histogram(np.array([0.5, 0.6]))
+    h = Histogram.normalized([1, 0, 3])
+    assert not h.full_support and h.n == 3 and h.min() == 0.0
+
+
+def test_balance_and_dual_md_step_spec():
+    mu = dxg.balance(dxg.LogOddsField(np.array([math.log(9.0), math.log(1.5)])), math.log(3.0))
+    assert np.allclose(mu.delta, [math.log(3.0), math.log(1.5)])
+    with pytest.raises(ValueError):
+        dxg.balance(mu, 0.0)
+    prm = dxg.DxgParams(eta=0.0, eta_mu=0.0, tau_p=1.0, tau_mu=1.0, beta=1.1, alpha=0.0)
+    out = dxg.dual_md_step(dxg.LogOddsField(np.zeros(2)), [0.6, 0.4], Histogram(np.array([0.5, 0.5])),
+                           [0.5, 0.5], prm)
+    assert np.allclose(out.delta, [0.8, -0.8])
+
+
+def test_infeasibility_report():
+    rep = infeasibility([0.6, 0.4], True, Histogram(np.array([0.5, 0.5])))
+    assert rep.row_gap == 0.0 and abs(rep.col_gap - 0.2) < 1e-15
+
+
+def test_dense_coupling_validation():
+    with pytest.raises(ValueError):
+        DenseCoupling(np.array([[0.5, -1e-3], [0.2, 0.3]]))
+    with pytest.raises(ValueError):
+        DenseCoupling(np.zeros((2, 3)))
+
+
+def test_solve_validates_before_touching_the_gpu():
+    class K:
+        n = 3
+    with pytest.raises(ValueError):
+        dxg.solve(K(), np.full(4, 0.25), np.full(3, 1 / 3), dxg.params_tuned())
+    prm = dxg.DxgParams(eta=0.0, eta_mu=0.0, tau_p=1.0, tau_mu=1.0, beta=1.1, alpha=0.0)
+    with pytest.raises(ValueError):
+        dxg.solve(K(), np.full(3, 1 / 3), np.array([0.5, 0.5, 0.0]), prm)
+
+
+def test_product_path_fails_loudly_without_cuda():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2511_11359_b200 import core
+    with pytest.raises(RuntimeError, match="CUDA"):
+        core.GridKernel(3, 3, 2)
