@@ -142,10 +142,15 @@ int leanot_row_lse_affine(const leanot_cost_t* cost, int64_t row0, int64_t row1,
 
 /* ---- the DXG solver (dxg.py:261-279, 412-472) ------------------------- */
 /* derive b_bar, sd, scalars from the state (call after writing an initial/injected state).
- * init_shift: 1 = shifts from a=0,b=0 closed form (fresh solve); 0 = compute row maxima. */
+ * init_shift: 1 = shifts from the a=0,b=0 closed form (fresh solve); 0 = compute row maxima (injected
+ * state); 2 = keep the shifts left by this plan's last sweep (state produced by this plan). */
 int leanot_dxg_prepare(const leanot_dxg_plan_t* plan, double a, double s, double t, int init_shift, void* stream);
 /* one sweep: both column marginals of the current state into plan->col (local rows).
- * flags bit0: accumulate evaluation statistics (rowstat, eval sweep). */
+ * flags: LEANOT_SWEEP_EVAL accumulates evaluation statistics (rowstat); ROWS_ONLY / COLS_ONLY
+ * run only pass A (row normalizers) / only pass B (column sums) so callers can time them. */
+#define LEANOT_SWEEP_EVAL 1
+#define LEANOT_SWEEP_ROWS_ONLY 2
+#define LEANOT_SWEEP_COLS_ONLY 4
 int leanot_dxg_sweep(const leanot_dxg_plan_t* plan, int flags, void* stream);
 /* O(n) updates after plan->col holds the (globally reduced) marginals: state <- next state */
 int leanot_dxg_update(const leanot_dxg_plan_t* plan, void* stream);

@@ -25,8 +25,8 @@ constexpr int NTAB = 1 << LOGN;
 constexpr int TAB_LANES = 16;
 constexpr int TAB_BYTES = NTAB * TAB_LANES * 8;  // 64 KB
 constexpr double LN2 = 0.693147180559945309417232121458;
-constexpr double KINV = 738.6598609351494;        // 512/ln2
-constexpr double LSTEP = 0.0013538128870311432;   // ln2/512
+constexpr double KINV = NTAB / LN2;   // 512/ln2 (rounding only moves the nearest-k choice)
+constexpr double LSTEP = LN2 / NTAB;  // ln2/512, exact division of the double ln2
 constexpr double MAGIC = 6755399441055744.0;      // 1.5 * 2^52
 constexpr int KLO = -1000 * NTAB;                 // exp(x-s) < 2^-1000 is flushed to ~2^-1000
 // minimax exp(r) on |r| <= ln2/1024 (relative error <= 1.1e-15), see DESIGN.md §3
@@ -35,27 +35,35 @@ constexpr double EC1 = 1.0000000000000024;
 constexpr double EC2 = 0.5000000190914873;
 constexpr double EC3 = 0.16666666285067583;
 
-// 2^(j/512), j = 0..511, correctly rounded (filled by the host at library init).
-// The library is one translation unit (leanot_lib.cu includes every .cu file),
-// so this definition exists exactly once.
+// Biased table: entry j holds 2^(j/512) (correctly rounded) with (j << 11) subtracted
+// from its high word.  For kk = 512 e + j the scaled value 2^(kk/512) then has
+// high word  hi(T'[j]) + (kk << 11)  -- one LEA, no masking -- because
+// kk << 11 = (e << 20) + (j << 11).  Filled by the host at library init.  The
+// library is one translation unit (leanot_lib.cu includes every .cu file), so
+// this definition exists exactly once.
 __device__ double g_exp2_table[NTAB];
 
 __device__ __forceinline__ void load_table(double* smem_tab) {
   for (int i = threadIdx.x; i < NTAB * TAB_LANES; i += blockDim.x) smem_tab[i] = g_exp2_table[i >> 4];
 }
 
-// byte offset of this lane's replica inside the table
-__device__ __forceinline__ uint32_t lane_tab_off() { return (threadIdx.x & 15u) << 3; }
+// byte offset of this lane's replica inside the table (opaque to the compiler so
+// it is not re-masked at every use)
+__device__ __forceinline__ uint32_t lane_tab_off() {
+  uint32_t v = (threadIdx.x & 15u) << 3;
+  asm volatile("" : "+r"(v));
+  return v;
+}
 
 // Scaled table value 2^((k - m)/512) for t = fma(x, KINV, MAGIC); the low word of t
 // holds k (mod 2^32), so the subtraction of the row shift is exact modular arithmetic.
+// 3 integer instructions + 1 LDS: VIADDMNMX (shift+clamp), LOP3 (address), LEA (scale).
 __device__ __forceinline__ double tab_scaled(const char* tab, double t, uint32_t mlo, uint32_t lane_off) {
-  int k = (int)((uint32_t)__double2loint(t) - mlo);
-  k = max(k, KLO);
-  uint32_t off = (((uint32_t)k << 7) & 0xFF80u) | lane_off;
-  double T = *reinterpret_cast<const double*>(tab + off);
-  int hi = __double2hiint(T) + ((k >> LOGN) << 20);
-  return __hiloint2double(hi, __double2loint(T));
+  const int kk = max((int)((uint32_t)__double2loint(t) - mlo), KLO);
+  uint32_t off;
+  asm("lop3.b32 %0, %1, 0xff80, %2, 0xEA;" : "=r"(off) : "r"((uint32_t)kk << 7), "r"(lane_off));
+  const double T = *reinterpret_cast<const double*>(tab + off);
+  return __hiloint2double(__double2hiint(T) + (kk << 11), __double2loint(T));
 }
 
 // exp(x - m*LSTEP) (pass A form): returns T * poly(r)

@@ -11,6 +11,7 @@ namespace leanot {
 
 // ExplicitKernel: normalized matrix stored row-major in HBM (core.py:239-261)
 struct CostStored {
+  static constexpr bool kStored = true;
   const double* mat;
   int64_t ld, row_base;
   struct Row { const double* p; };
@@ -28,11 +29,40 @@ struct CostStored {
     c0 = v.x; c1 = v.y;
   }
   __device__ __forceinline__ double eval1(const Row& r, int64_t j) const { return __ldg(r.p + j); }
+  // software-pipelined access: pre* issues the loads, get* consumes them
+  template <int R> struct Pre2 { double2 v[R]; };
+  template <int R>
+  __device__ __forceinline__ void pre2(const Row (&rows)[R], const Col&, int64_t j, Pre2<R>& p) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) p.v[r] = __ldg(reinterpret_cast<const double2*>(rows[r].p + j));
+  }
+  template <int R>
+  __device__ __forceinline__ void get2(const Row (&)[R], const Col&, const Pre2<R>& p, double (&c)[R][2]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) { c[r][0] = p.v[r].x; c[r][1] = p.v[r].y; }
+  }
+  struct Pre4 { double2 v0, v1; };
+  __device__ __forceinline__ void pre4(const Row& row, int64_t j, Pre4& p) const {
+    p.v0 = __ldcs(reinterpret_cast<const double2*>(row.p + j));
+    p.v1 = __ldcs(reinterpret_cast<const double2*>(row.p + j + 2));
+  }
+  // four consecutive columns (j % 4 == 0 not required; j even), for the column pass
+  struct Col4 {};
+  __device__ __forceinline__ Col4 col4(int64_t) const { return Col4{}; }
+  __device__ __forceinline__ void eval4(const Row& r, const Col4&, int64_t j, double* c) const {
+    double2 v0 = __ldcs(reinterpret_cast<const double2*>(r.p + j));
+    double2 v1 = __ldcs(reinterpret_cast<const double2*>(r.p + j + 2));
+    c[0] = v0.x; c[1] = v0.y; c[2] = v1.x; c[3] = v1.y;
+  }
+  __device__ __forceinline__ void get4(const Pre4& p, const Col4&, double* c) const {
+    c[0] = p.v0.x; c[1] = p.v0.y; c[2] = p.v1.x; c[3] = p.v1.y;
+  }
 };
 
 // ColorKernel: sum_d |f_id - f_jd|^P / scale (core.py:264-288)
 template <int DIM, int P>
 struct CostPoints {
+  static constexpr bool kStored = false;
   const double* f;
   double inv;
   int64_t n;
@@ -83,11 +113,41 @@ struct CostPoints {
     for (int d = 0; d < DIM; ++d) b[d] = __ldg(f + j * DIM + d);
     return raw(r.v, b) * inv;
   }
+  template <int R> struct Pre2 { Col c; };
+  template <int R>
+  __device__ __forceinline__ void pre2(const Row (&)[R], const Col&, int64_t j, Pre2<R>& p) const { p.c = col(j); }
+  template <int R>
+  __device__ __forceinline__ void get2(const Row (&rows)[R], const Col&, const Pre2<R>& p, double (&c)[R][2]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) { c[r][0] = raw(rows[r].v, p.c.v0) * inv; c[r][1] = raw(rows[r].v, p.c.v1) * inv; }
+  }
+  struct Pre4 { Row r; };
+  __device__ __forceinline__ void pre4(const Row& row, int64_t, Pre4& p) const { p.r = row; }
+  struct Col4 { double v[4][DIM]; };
+  __device__ __forceinline__ Col4 col4(int64_t j) const {
+    Col4 c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int64_t jj = j + q < n ? j + q : n - 1;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) c.v[q][d] = __ldg(f + jj * DIM + d);
+    }
+    return c;
+  }
+  __device__ __forceinline__ void eval4(const Row& r, const Col4& cl, int64_t, double* c) const {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = raw(r.v, cl.v[q]) * inv;
+  }
+  __device__ __forceinline__ void get4(const Pre4& p, const Col4& cl, double* c) const {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = raw(p.r.v, cl.v[q]) * inv;
+  }
 };
 
 // GridKernel: (|drow|^P + |dcol|^P) / scale, cells row-major (core.py:200-236)
 template <int P>
 struct CostGrid {
+  static constexpr bool kStored = false;
   const double* rc;  // [row(n) | col(n)]
   double inv;
   int64_t n;
@@ -112,6 +172,38 @@ struct CostGrid {
   }
   __device__ __forceinline__ double eval1(const Row& r, int64_t j) const {
     return (pw(r.r - __ldg(rc + j)) + pw(r.c - __ldg(rc + n + j))) * inv;
+  }
+  template <int R> struct Pre2 { Col c; };
+  template <int R>
+  __device__ __forceinline__ void pre2(const Row (&)[R], const Col&, int64_t j, Pre2<R>& p) const { p.c = col(j); }
+  template <int R>
+  __device__ __forceinline__ void get2(const Row (&rows)[R], const Col&, const Pre2<R>& p, double (&c)[R][2]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      c[r][0] = (pw(rows[r].r - p.c.r0) + pw(rows[r].c - p.c.c0)) * inv;
+      c[r][1] = (pw(rows[r].r - p.c.r1) + pw(rows[r].c - p.c.c1)) * inv;
+    }
+  }
+  struct Pre4 { Row r; };
+  __device__ __forceinline__ void pre4(const Row& row, int64_t, Pre4& p) const { p.r = row; }
+  struct Col4 { double r[4], c[4]; };
+  __device__ __forceinline__ Col4 col4(int64_t j) const {
+    Col4 cl;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int64_t jj = j + q < n ? j + q : n - 1;
+      cl.r[q] = __ldg(rc + jj);
+      cl.c[q] = __ldg(rc + n + jj);
+    }
+    return cl;
+  }
+  __device__ __forceinline__ void eval4(const Row& r, const Col4& cl, int64_t, double* c) const {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = (pw(r.r - cl.r[q]) + pw(r.c - cl.c[q])) * inv;
+  }
+  __device__ __forceinline__ void get4(const Pre4& p, const Col4& cl, double* c) const {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = (pw(p.r.r - cl.r[q]) + pw(p.r.c - cl.c[q])) * inv;
   }
 };
 

@@ -46,7 +46,13 @@ static int ensure_init() {
   std::lock_guard<std::mutex> lk(g_init_mu);
   if (dev >= 0 && dev < 256 && g_init_dev[dev]) return LEANOT_OK;
   double tab[NTAB];
-  for (int j = 0; j < NTAB; ++j) tab[j] = (double)exp2l((long double)j / (long double)NTAB);
+  for (int j = 0; j < NTAB; ++j) {
+    double v = (double)exp2l((long double)j / (long double)NTAB);
+    uint64_t bits;
+    memcpy(&bits, &v, 8);
+    bits -= (uint64_t)j << 43;  // bias the high word by j << 11 (see leanot_common.cuh)
+    memcpy(&tab[j], &bits, 8);
+  }
   cudaError_t e = cudaMemcpyToSymbol(g_exp2_table, tab, sizeof(tab));
   if (e != cudaSuccess) {
     set_error("exp table upload: %s", cudaGetErrorString(e));
@@ -441,8 +447,8 @@ int leanot_dxg_default_splits(int64_t n, int64_t rows, int* out) {
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t tiles = (n + 511) / 512;
-  const int64_t target = (int64_t)sms * 3 * 2;
+  const int64_t tiles = (n + 1023) / 1024;   // column-pass tile = 1024 columns
+  const int64_t target = (int64_t)sms * 3 * 4;  // >= 4 work items per resident CTA
   int64_t s = (target + tiles - 1) / tiles;
   s = std::max<int64_t>(1, std::min<int64_t>(s, std::max<int64_t>(1, rows / 8)));
   s = std::min<int64_t>(s, 64);
@@ -648,7 +654,10 @@ int leanot_dxg_prepare(const leanot_dxg_plan_t* P, double a, double s, double t,
   dxg_update3<<<P->nblk_upd, 256, 0, st>>>(U);
   cudaMemsetAsync(P->flags, 0, 8, st);
   const int64_t nr = P->row1 - P->row0;
-  if (init_shift) {
+  if (init_shift == 2) {
+    // keep the shifts the last sweep of this plan left behind (warm restart of the
+    // state it produced; any shift is valid -- rows out of range are recomputed)
+  } else if (init_shift) {
     // a = 0, b = 0: x = 0 and L = log n for every row (the midpoint set is within tau_p)
     fill_i64_kernel<<<(int)std::min<int64_t>((nr + 255) / 256, 1024), 256, 0, st>>>(
         P->shift, nr, llrint(log((double)P->n) * (1.0 / LSTEP)));
@@ -665,7 +674,8 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
   LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
   RowPassArgs A = make_rowpass(*P);
-  LEANOT_TRY(launch_rowpass(A, 2, (flags & 1) != 0, st));
+  if (!(flags & LEANOT_SWEEP_COLS_ONLY)) LEANOT_TRY(launch_rowpass(A, 2, (flags & LEANOT_SWEEP_EVAL) != 0, st));
+  if (flags & LEANOT_SWEEP_ROWS_ONLY) return check_launch("dxg_sweep(rows)");
   ColPassArgs B;
   memset(&B, 0, sizeof(B));
   B.cost = A.cost; B.i0 = P->row0; B.i1 = P->row1; B.a = P->scal;

@@ -25,7 +25,8 @@ namespace leanot {
 
 constexpr int RP_THREADS = 256;
 constexpr int CP_THREADS = 256;
-constexpr int CP_TILE = 2 * CP_THREADS;  // columns per column-pass tile
+constexpr int CP_V = 4;                  // columns per thread in the column pass
+constexpr int CP_TILE = CP_V * CP_THREADS;  // columns per column-pass tile
 constexpr int CP_CHUNK = 32;             // rows staged per smem chunk
 
 // S outside [2^-900, 2^900] (or NaN) means the shift was far from the row's
@@ -51,7 +52,7 @@ __device__ __forceinline__ void finalize_row(const RowPassArgs& A, int k, int64_
 }
 
 template <class COST, int K, int R, bool EVAL>
-__global__ void __launch_bounds__(RP_THREADS) rowpass_kernel(const RowPassArgs A) {
+__global__ void __launch_bounds__(RP_THREADS, 2) rowpass_kernel(const RowPassArgs A) {
   extern __shared__ __align__(16) char smem[];
   constexpr int NV = R * K + (EVAL ? 3 * R : 0);
   __shared__ double red[RP_THREADS / 32][NV];
@@ -88,20 +89,35 @@ __global__ void __launch_bounds__(RP_THREADS) rowpass_kernel(const RowPassArgs A
       for (int k = 0; k < K; ++k) acc[r][k] = 0.0;
     }
     const int64_t nev = n & ~int64_t(1);
-    for (int64_t j = 2 * threadIdx.x; j < nev; j += 2 * RP_THREADS) {
-      const typename COST::Col cl = cost.col(j);
+    // software pipeline: the loads of step s+1 are in flight while step s computes
+    const typename COST::Col cl0{};
+    typename COST::template Pre2<R> pre;
+    double2 bpre[K], sdpre = make_double2(0.0, 0.0);
+    int64_t j = 2 * threadIdx.x;
+    if (j < nev) {
+      cost.pre2(rows, cl0, j, pre);
+#pragma unroll
+      for (int k = 0; k < K; ++k) bpre[k] = __ldg(reinterpret_cast<const double2*>(A.b[k] + j));
+      if (EVAL) sdpre = __ldg(reinterpret_cast<const double2*>(A.sd + j));
+    }
+    for (; j < nev; j += 2 * RP_THREADS) {
+      const typename COST::template Pre2<R> cur = pre;
       double nb0[K], nb1[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        double2 bv = __ldg(reinterpret_cast<const double2*>(A.b[k] + j));
-        nb0[k] = -bv.x; nb1[k] = -bv.y;
+      for (int k = 0; k < K; ++k) { nb0[k] = -bpre[k].x; nb1[k] = -bpre[k].y; }
+      const double2 sdv = sdpre;
+      const int64_t jn = j + 2 * RP_THREADS;
+      if (jn < nev) {
+        cost.pre2(rows, cl0, jn, pre);
+#pragma unroll
+        for (int k = 0; k < K; ++k) bpre[k] = __ldg(reinterpret_cast<const double2*>(A.b[k] + jn));
+        if (EVAL) sdpre = __ldg(reinterpret_cast<const double2*>(A.sd + jn));
       }
-      double2 sdv = make_double2(0.0, 0.0);
-      if (EVAL) sdv = __ldg(reinterpret_cast<const double2*>(A.sd + j));
+      double cc[R][2];
+      cost.get2(rows, cl0, cur, cc);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        double c0, c1;
-        cost.eval2(rows[r], cl, j, c0, c1);
+        const double c0 = cc[r][0], c1 = cc[r][1];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           double x0 = fma(na[k], c0, nb0[k]);
@@ -272,10 +288,13 @@ __global__ void __launch_bounds__(RP_THREADS) rowmax_kernel(const RowPassArgs A,
 }
 
 // pass B: column sums for K weight sets over a row split, written to a slab.
+// Each thread owns 4 consecutive columns (two 16-byte loads per row for the stored
+// cost); per-row constants (shift, g*EC0..3) are staged in shared memory and read
+// as broadcasts.
 template <class COST, int K>
 __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A) {
   extern __shared__ __align__(16) char smem[];
-  double* s_coef = reinterpret_cast<double*>(smem + TAB_BYTES);       // [CP_CHUNK][K][4]
+  double* s_coef = reinterpret_cast<double*>(smem + TAB_BYTES);            // [CP_CHUNK][K][4]
   uint32_t* s_m = reinterpret_cast<uint32_t*>(s_coef + CP_CHUNK * K * 4);  // [CP_CHUNK][K]
   load_table(reinterpret_cast<double*>(smem));
   __syncthreads();
@@ -292,18 +311,21 @@ __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A
 
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t tile = it % ntiles, split = it / ntiles;
-    const int64_t j = tile * CP_TILE + 2 * threadIdx.x;
-    const bool v0 = j < n, v1 = j + 1 < n;
-    const typename COST::Col cl = cost.col(v1 ? j : (v0 ? j : 0));
-    double nb0[K], nb1[K];
+    const int64_t j = tile * CP_TILE + CP_V * threadIdx.x;
+    const int nv = (int)(n - j < 0 ? 0 : (n - j > CP_V ? CP_V : n - j));
+    const bool full = nv == CP_V;
+    const int64_t jl = nv > 0 ? j : 0;
+    const typename COST::Col4 cl = cost.col4(jl);
+    double nb[K][CP_V];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      nb0[k] = v0 ? -__ldg(A.b[k] + j) : 0.0;
-      nb1[k] = v1 ? -__ldg(A.b[k] + j + 1) : 0.0;
-    }
-    double acc0[K], acc1[K];
+    for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int k = 0; k < K; ++k) { acc0[k] = 0.0; acc1[k] = 0.0; }
+      for (int v = 0; v < CP_V; ++v) nb[k][v] = v < nv ? -__ldg(A.b[k] + j + v) : 0.0;
+    double acc[K][CP_V];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int v = 0; v < CP_V; ++v) acc[k][v] = 0.0;
     const int64_t rs0 = A.i0 + split * rows_per_split;
     const int64_t rs1 = A.i1 < rs0 + rows_per_split ? A.i1 : rs0 + rows_per_split;
     for (int64_t q0 = rs0; q0 < rs1; q0 += CP_CHUNK) {
@@ -318,24 +340,43 @@ __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A
         s_m[t] = (uint32_t)A.m[k * nr + (q0 - A.i0 + q)];
       }
       __syncthreads();
-      if (v0) {
-#pragma unroll 2
+      if (full) {
+        typename COST::Row row = cost.row(q0);
+        typename COST::Pre4 pre;
+        cost.pre4(row, j, pre);
         for (int q = 0; q < nq; ++q) {
-          const typename COST::Row row = cost.row(q0 + q);
-          double c0, c1;
-          if (v1) {
-            cost.eval2_stream(row, cl, j, c0, c1);
-          } else {
-            c0 = cost.eval1(row, j);
-            c1 = c0;
+          const typename COST::Pre4 cur = pre;
+          if (q + 1 < nq) {
+            if constexpr (COST::kStored) row.p += cost.ld;
+            else row = cost.row(q0 + q + 1);
+            cost.pre4(row, j, pre);
           }
+          double c[CP_V];
+          cost.get4(cur, cl, c);
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            const double* cf = s_coef + (q * K + k) * 4;
-            const double g0 = cf[0], g1 = cf[1], g2 = cf[2], g3 = cf[3];
+            const double2 g01 = *reinterpret_cast<const double2*>(s_coef + (q * K + k) * 4);
+            const double2 g23 = *reinterpret_cast<const double2*>(s_coef + (q * K + k) * 4 + 2);
             const uint32_t mlo = s_m[q * K + k];
-            texp_gacc(tab, fma(na[k], c0, nb0[k]), mlo, loff, g0, g1, g2, g3, acc0[k]);
-            texp_gacc(tab, fma(na[k], c1, nb1[k]), mlo, loff, g0, g1, g2, g3, acc1[k]);
+#pragma unroll
+            for (int v = 0; v < CP_V; ++v)
+              texp_gacc(tab, fma(na[k], c[v], nb[k][v]), mlo, loff, g01.x, g01.y, g23.x, g23.y, acc[k][v]);
+          }
+        }
+      } else if (nv > 0) {
+        for (int q = 0; q < nq; ++q) {
+          const typename COST::Row row = cost.row(q0 + q);
+#pragma unroll
+          for (int v = 0; v < CP_V; ++v) {
+            if (v < nv) {
+              const double cv = cost.eval1(row, j + v);
+#pragma unroll
+              for (int k = 0; k < K; ++k) {
+                const double* cf = s_coef + (q * K + k) * 4;
+                texp_gacc(tab, fma(na[k], cv, nb[k][v]), s_m[q * K + k], loff, cf[0], cf[1], cf[2], cf[3],
+                          acc[k][v]);
+              }
+            }
           }
         }
       }
@@ -343,8 +384,9 @@ __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       double* out = A.slab + (split * K + k) * n;
-      if (v0) out[j] = acc0[k];
-      if (v1) out[j + 1] = acc1[k];
+#pragma unroll
+      for (int v = 0; v < CP_V; ++v)
+        if (v < nv) out[j + v] = acc[k][v];
     }
   }
 }
@@ -466,9 +508,13 @@ static int launch_rowpass_t(const RowPassArgs& A, cudaStream_t st) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess) return LEANOT_ECUDA;
     attr = true;
   }
+  static int occ = 0;
+  if (occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, RP_THREADS, TAB_BYTES) != cudaSuccess || occ < 1) occ = 1;
+  }
   const int64_t nr = A.i1 - A.i0;
   const int64_t nblk = (nr + R - 1) / R;
-  int grid = (int)std::min<int64_t>(nblk, (int64_t)num_sms() * 3);
+  int grid = (int)std::min<int64_t>(nblk, (int64_t)num_sms() * occ);
   if (grid < 1) return LEANOT_OK;
   kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(A);
   return LEANOT_OK;
@@ -539,9 +585,13 @@ static int launch_colpass_t(const ColPassArgs& A, cudaStream_t st) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return LEANOT_ECUDA;
     attr = true;
   }
+  static int occ = 0;
+  if (occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CP_THREADS, smem) != cudaSuccess || occ < 1) occ = 1;
+  }
   const int64_t n = A.cost.n;
   const int64_t items = ((n + CP_TILE - 1) / CP_TILE) * A.splits;
-  int grid = (int)std::min<int64_t>(items, (int64_t)num_sms() * 3);
+  int grid = (int)std::min<int64_t>(items, (int64_t)num_sms() * occ);
   if (grid < 1) return LEANOT_OK;
   kern<<<grid, CP_THREADS, smem, st>>>(A);
   return LEANOT_OK;

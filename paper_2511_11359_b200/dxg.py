@@ -279,18 +279,38 @@ def _engine_for(kernel, r, c, params) -> DxgEngine:
     return DxgEngine(kernel, as_weights(r), as_weights(c), params, group=default_group())
 
 
+# One cached engine for repeated dxg_step calls on the same (kernel, r, c, params):
+# buffers stay allocated and, when the caller passes back the state the previous
+# call returned, the row shifts of that sweep are reused (no row-max pass).
+_STEP_CACHE: dict = {}
+
+
 def dxg_step(state: DxgState, kernel: CostKernel, r: Histogram, c: Histogram, params: DxgParams,
              workers: int = 1) -> DxgState:
-    """One extragradient iteration (dxg.py:261-279): one device sweep + fused O(n) update."""
+    """One extragradient iteration (dxg.py:261-279): one device sweep + fused O(n) update.
+
+    Host state in, host state out: the state is copied H2D, iterated in HBM and
+    copied back (the reference-facing call with host buffers).
+    """
     kernel = _dev_kernel(kernel)
-    eng = _engine_for(kernel, r, c, params)
+    key = (id(kernel), id(r), id(c), params)
+    ent = _STEP_CACHE.get("entry")
+    if ent is None or ent["key"] != key:
+        _STEP_CACHE.clear()
+        ent = {"key": key, "refs": (kernel, r, c), "eng": _engine_for(kernel, r, c, params), "last": None}
+        _STEP_CACHE["entry"] = ent
+    eng = ent["eng"]
     w = state.weights
-    eng.load_state(state.mu.delta, w.b, w.a, w.s, w.t, fresh=False)
+    last = ent["last"]
+    warm = (last is not None and (w.a, w.s, w.t) == last[2] and np.array_equal(state.mu.delta, last[0])
+            and np.array_equal(w.b, last[1]))
+    eng.load_state(state.mu.delta, w.b, w.a, w.s, w.t, keep_shift=warm)
     eng.sweep()
     eng.update()
     delta, b, a, s, t = eng.read_state()
-    eng.close()
-    return DxgState(LogOddsField(delta), TransportLogWeights(a=a, b=b, s=s, t=int(w.t) + 1))
+    out = DxgState(LogOddsField(delta), TransportLogWeights(a=a, b=b, s=s, t=int(w.t) + 1))
+    ent["last"] = (delta, b, (a, s, int(w.t) + 1))
+    return out
 
 
 def _plan_stats(state: TransportLogWeights, kernel: CostKernel, r: Histogram, workers: int = 1):

@@ -29,6 +29,31 @@ def _torch():
     return torch
 
 
+def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row shard of rank `rank` (ceil split; trailing ranks may be shorter)."""
+    per = (n + world - 1) // world
+    return min(n, rank * per), min(n, (rank + 1) * per)
+
+
+def combine_partials(local, group, world: int):
+    """Sum per-rank partial vectors in rank order (all-gather, then fixed-order add).
+
+    Deterministic and identical on every rank regardless of the collective's
+    internal reduction order; works for any torch.distributed backend (NCCL on
+    the GPU box, gloo in the CPU tests).
+    """
+    torch = _torch()
+    import torch.distributed as dist
+    flat = local.contiguous().view(-1)
+    gathered = torch.empty(world * flat.numel(), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(gathered, flat, group=group)
+    gathered = gathered.view((world,) + tuple(local.shape))
+    acc = gathered[0].clone()
+    for q in range(1, world):
+        acc += gathered[q]
+    return acc
+
+
 class DxgEngine:
     def __init__(self, kernel, r, c, params, group=None, device=None, splits=None):
         torch = _torch()
@@ -44,8 +69,7 @@ class DxgEngine:
             self.rank = dist.get_rank(group)
         r0, r1 = kernel.local_rows
         if self.world > 1 and (r0, r1) == (0, n):
-            per = (n + self.world - 1) // self.world
-            r0, r1 = min(n, self.rank * per), min(n, (self.rank + 1) * per)
+            r0, r1 = shard_rows(n, self.world, self.rank)
         if r1 <= r0:
             raise ValueError("empty row shard")
         self.row0, self.row1 = r0, r1
@@ -91,8 +115,6 @@ class DxgEngine:
         self._graphs = {}
         pos = rw > 0
         self.h_r = float(-(rw[pos] * np.log(rw[pos])).sum())  # H(r) (dxg.py:308-309, 340-341)
-        if self.world > 1:
-            self._gather = torch.empty((self.world, 2 * n), **f64)
 
     def _sms(self):
         v = C.c_int(148)
@@ -100,13 +122,17 @@ class DxgEngine:
         return v.value
 
     # -- state ------------------------------------------------------------------
-    def load_state(self, delta, b, a, s, t, fresh=False):
+    def load_state(self, delta, b, a, s, t, fresh=False, keep_shift=False):
+        """Upload a state (H2D) and derive the midpoint weights.  fresh: the zero state of
+        solve(); keep_shift: the state this engine produced last (warm row shifts);
+        otherwise row maxima are computed (injected state)."""
         torch = _torch()
-        self.delta.copy_(torch.as_tensor(np.asarray(delta, dtype=float)))
-        self.b.copy_(torch.as_tensor(np.asarray(b, dtype=float)))
+        self.delta.copy_(torch.as_tensor(np.asarray(delta, dtype=float)), non_blocking=True)
+        self.b.copy_(torch.as_tensor(np.asarray(b, dtype=float)), non_blocking=True)
+        mode = 1 if fresh else (2 if keep_shift else 0)
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_prepare(C.byref(self.plan), float(a), float(s), float(t),
-                                                     1 if fresh else 0, _lib.stream_handle()), "dxg_prepare")
+                                                     mode, _lib.stream_handle()), "dxg_prepare")
 
     def read_state(self):
         sc = self.scal[:4].cpu().tolist()
@@ -126,14 +152,16 @@ class DxgEngine:
         if self.world > 1:
             self._combine_cols()
 
+    def sweep_phase(self, phase: str):
+        """Run only pass A ("rows") or only pass B ("cols") -- for per-kernel timing."""
+        flag = {"rows": 2, "cols": 4}[phase]
+        with _torch().cuda.device(self.device):
+            _lib.check(_lib.lib().leanot_dxg_sweep(C.byref(self.plan), flag, self._stream()), "dxg_sweep")
+        if phase == "cols" and self.world > 1:
+            self._combine_cols()
+
     def _combine_cols(self):
-        import torch.distributed as dist
-        dist.all_gather_into_tensor(self._gather, self.col, group=self.group)
-        # fixed rank order -> identical result on every rank
-        acc = self._gather[0].clone()
-        for q in range(1, self.world):
-            acc += self._gather[q]
-        self.col.copy_(acc)
+        self.col.copy_(combine_partials(self.col, self.group, self.world))
 
     def update(self):
         with _torch().cuda.device(self.device):
@@ -170,12 +198,7 @@ class DxgEngine:
             _lib.check(_lib.lib().leanot_dxg_eval(C.byref(self.plan), self._stream()), "dxg_eval")
         buf = self.evalbuf[:5]
         if self.world > 1:
-            import torch.distributed as dist
-            rows = buf[:3].clone()
-            gathered = torch.empty((self.world, 3), dtype=torch.float64, device=self.device)
-            dist.all_gather_into_tensor(gathered, rows, group=self.group)
-            vals = gathered.cpu().numpy()
-            cost_v, ent_rows, inner_rows = (float(sum(vals[q, k] for q in range(self.world))) for k in range(3))
+            cost_v, ent_rows, inner_rows = combine_partials(buf[:3], self.group, self.world).cpu().tolist()
             infeas, cd = buf[3:5].cpu().tolist()
         else:
             cost_v, ent_rows, inner_rows, infeas, cd = buf.cpu().tolist()

@@ -79,10 +79,17 @@ def test_dxg_step_injected_state(name, scheme):
     assert [nxt.weights.a, nxt.weights.s, nxt.weights.t] == d[f"{scheme}_out_scalars"].tolist()
 
 
+# Per-iteration horizons: params_li (tau_mu ~ 450) amplifies rounding noise the way
+# tuned tau_mu=1 does -- the reference itself, with only its row-block size changed,
+# leaves 1e-10 after ~20 iterations (tests/test_oracle_noise.py) -- so li is compared
+# over its first 12 iterations; the other regimes over all 40.
+HORIZON = {"tuned_taumu005": 40, "loose": 40, "tuned_eta1e-3": 40, "li": 12}
+
+
 @pytest.mark.parametrize("name", STEPS)
 @pytest.mark.parametrize("scheme", ["tuned_taumu005", "loose", "li", "tuned_eta1e-3"])
 def test_trajectory_per_iteration(name, scheme):
-    """40 iterations from the zero state through the solver engine, every iterate within 1e-10."""
+    """Iterations from the zero state through the solver engine, every iterate within 1e-10."""
     from paper_2511_11359_b200.engine import DxgEngine
     d = load(name)
     k = device_cost(d)
@@ -91,12 +98,14 @@ def test_trajectory_per_iteration(name, scheme):
     eng = DxgEngine(k, d["r"], d["c"], prm)
     n = k.n
     eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
-    for it in range(d[f"{scheme}_traj_delta"].shape[0]):
+    steps = d[f"{scheme}_traj_delta"].shape[0]
+    for it in range(steps):
         eng.sweep()
         eng.update()
         delta, b, a, s, t = eng.read_state()
-        assert rel_err(delta, d[f"{scheme}_traj_delta"][it]) <= TOL_ITER, it
-        assert rel_err(b, d[f"{scheme}_traj_b"][it]) <= TOL_ITER, it
+        if it < HORIZON[scheme]:
+            assert rel_err(delta, d[f"{scheme}_traj_delta"][it]) <= TOL_ITER, it
+            assert rel_err(b, d[f"{scheme}_traj_b"][it]) <= TOL_ITER, it
     assert [a, s, t] == d[f"{scheme}_traj_scalars"].tolist()
 
 
@@ -183,3 +192,28 @@ def test_large_dynamic_range_shift_fixup():
         col = dxg.column_marginal(dxg.TransportLogWeights(a, b, 0.0, 0), k, r)
         (ref,) = O.column_marginals(O.DenseCost(Cm), r, [(a, b)])
         assert rel_err(col, ref) <= 1e-11
+
+
+def test_config1_same_iteration_count_as_reference():
+    """BASELINE config 1 end to end: n=1000 random C, tuned + tau_mu=0.05, eps=1e-4.
+
+    The reference converges at iteration 8,225 (tests/golden/config1_n1000.npz)."""
+    dxg = _dxg()
+    from paper_2511_11359_b200 import core
+    d = load("config1_n1000")
+    n = 1000
+    rng = np.random.default_rng(0)
+    r = core.Histogram.normalized(rng.random(n))
+    c = core.Histogram.normalized(rng.random(n))
+    Cm = rng.random((n, n))
+    k = core.ExplicitKernel(Cm)
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    sol = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-4), log_stride=25, dense_cap=0)
+    assert sol.converged and sol.iterations == int(d["iterations"]) == 8225
+    ref = d["traj"]
+    got = np.array([[p.iter, p.primal, p.dual, p.gap, p.col_infeas_l1, p.s] for p in sol.trajectory])
+    assert got.shape == ref.shape
+    assert rel_err(got[:, 1], ref[:, 1]) <= 1e-8
+    assert rel_err(got[:, 2], ref[:, 2]) <= 1e-8
+    assert abs(sol.final.primal - ref[-1, 1]) <= 1e-8 * abs(ref[-1, 1])   # final transport cost
+    assert rel_err(sol.state.mu.delta, d["delta"]) <= 1e-8
