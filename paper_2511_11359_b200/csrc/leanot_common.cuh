@@ -47,53 +47,55 @@ __device__ __forceinline__ void load_table(double* smem_tab) {
   for (int i = threadIdx.x; i < NTAB * TAB_LANES; i += blockDim.x) smem_tab[i] = g_exp2_table[i >> 4];
 }
 
-// byte offset of this lane's replica inside the table (opaque to the compiler so
-// it is not re-masked at every use)
-__device__ __forceinline__ uint32_t lane_tab_off() {
-  uint32_t v = (threadIdx.x & 15u) << 3;
+// Shared-window address of this lane's replica of the table (base + lane*8), opaque
+// to the compiler so it is kept in one register instead of being re-derived.
+__device__ __forceinline__ uint32_t lane_tab_addr(const void* smem_tab) {
+  uint32_t v = (uint32_t)__cvta_generic_to_shared(smem_tab) + ((threadIdx.x & 15u) << 3);
   asm volatile("" : "+r"(v));
   return v;
 }
 
 // Scaled table value 2^((k - m)/512) for t = fma(x, KINV, MAGIC); the low word of t
 // holds k (mod 2^32), so the subtraction of the row shift is exact modular arithmetic.
-// 3 integer instructions + 1 LDS: VIADDMNMX (shift+clamp), LOP3 (address), LEA (scale).
-__device__ __forceinline__ double tab_scaled(const char* tab, double t, uint32_t mlo, uint32_t lane_off) {
+// 4 integer instructions + 1 LDS: VIADDMNMX (shift+clamp), LOP3 (j = kk & 511),
+// LEA (address), IMAD (exponent add, biased table).
+__device__ __forceinline__ double tab_scaled(uint32_t tb, double t, uint32_t mlo) {
   const int kk = max((int)((uint32_t)__double2loint(t) - mlo), KLO);
-  uint32_t off;
-  asm("lop3.b32 %0, %1, 0xff80, %2, 0xEA;" : "=r"(off) : "r"((uint32_t)kk << 7), "r"(lane_off));
-  const double T = *reinterpret_cast<const double*>(tab + off);
+  double T;
+  asm("{\n\t.reg .b32 j, a;\n\tand.b32 j, %1, 511;\n\tmad.lo.u32 a, j, 128, %2;\n\t"
+      "ld.shared.f64 %0, [a];\n\t}"
+      : "=d"(T) : "r"(kk), "r"(tb));
   return __hiloint2double(__double2hiint(T) + (kk << 11), __double2loint(T));
 }
 
 // exp(x - m*LSTEP) (pass A form): returns T * poly(r)
-__device__ __forceinline__ double texp(const char* tab, double x, uint32_t mlo, uint32_t lane_off) {
-  double t = fma(x, KINV, MAGIC);
-  double kd = t - MAGIC;
-  double r = fma(kd, -LSTEP, x);
-  double T = tab_scaled(tab, t, mlo, lane_off);
-  double p = fma(fma(EC3, r, EC2), r, EC1);
+__device__ __forceinline__ double texp(uint32_t tb, double x, uint32_t mlo) {
+  const double t = fma(x, KINV, MAGIC);
+  const double kd = t - MAGIC;
+  const double r = fma(kd, -LSTEP, x);
+  const double T = tab_scaled(tb, t, mlo);
+  const double p = fma(fma(EC3, r, EC2), r, EC1);
   return T * fma(r, p, EC0);
 }
 
 // acc += exp(x - m*LSTEP)
-__device__ __forceinline__ void texp_acc(const char* tab, double x, uint32_t mlo, uint32_t lane_off, double& acc) {
-  double t = fma(x, KINV, MAGIC);
-  double kd = t - MAGIC;
-  double r = fma(kd, -LSTEP, x);
-  double T = tab_scaled(tab, t, mlo, lane_off);
-  double p = fma(fma(EC3, r, EC2), r, EC1);
+__device__ __forceinline__ void texp_acc(uint32_t tb, double x, uint32_t mlo, double& acc) {
+  const double t = fma(x, KINV, MAGIC);
+  const double kd = t - MAGIC;
+  const double r = fma(kd, -LSTEP, x);
+  const double T = tab_scaled(tb, t, mlo);
+  const double p = fma(fma(EC3, r, EC2), r, EC1);
   acc = fma(T, fma(r, p, EC0), acc);
 }
 
 // acc += g * exp(x - m*LSTEP) with g folded into the polynomial: gc = g*{EC0..EC3}
-__device__ __forceinline__ void texp_gacc(const char* tab, double x, uint32_t mlo, uint32_t lane_off,
-                                          double g0, double g1, double g2, double g3, double& acc) {
-  double t = fma(x, KINV, MAGIC);
-  double kd = t - MAGIC;
-  double r = fma(kd, -LSTEP, x);
-  double T = tab_scaled(tab, t, mlo, lane_off);
-  double q = fma(fma(fma(g3, r, g2), r, g1), r, g0);
+__device__ __forceinline__ void texp_gacc(uint32_t tb, double x, uint32_t mlo, double g0, double g1, double g2,
+                                          double g3, double& acc) {
+  const double t = fma(x, KINV, MAGIC);
+  const double kd = t - MAGIC;
+  const double r = fma(kd, -LSTEP, x);
+  const double T = tab_scaled(tb, t, mlo);
+  const double q = fma(fma(fma(g3, r, g2), r, g1), r, g0);
   acc = fma(T, q, acc);
 }
 

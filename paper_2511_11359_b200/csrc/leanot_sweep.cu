@@ -27,7 +27,7 @@ constexpr int RP_THREADS = 256;
 constexpr int CP_THREADS = 256;
 constexpr int CP_V = 4;                  // columns per thread in the column pass
 constexpr int CP_TILE = CP_V * CP_THREADS;  // columns per column-pass tile
-constexpr int CP_CHUNK = 32;             // rows staged per smem chunk
+constexpr int CP_CHUNK = 128;            // rows staged per smem chunk
 
 // S outside [2^-900, 2^900] (or NaN) means the shift was far from the row's
 // log-normalizer: the row is recomputed with an exact max shift (fixup_kernel).
@@ -58,8 +58,7 @@ __global__ void __launch_bounds__(RP_THREADS, 2) rowpass_kernel(const RowPassArg
   __shared__ double red[RP_THREADS / 32][NV];
   load_table(reinterpret_cast<double*>(smem));
   __syncthreads();
-  const char* tab = smem;
-  const uint32_t loff = lane_tab_off();
+  const uint32_t tb = lane_tab_addr(smem);
   const COST cost(A.cost);
   const int64_t n = A.cost.n;
   const int64_t nr = A.i1 - A.i0;
@@ -89,53 +88,52 @@ __global__ void __launch_bounds__(RP_THREADS, 2) rowpass_kernel(const RowPassArg
       for (int k = 0; k < K; ++k) acc[r][k] = 0.0;
     }
     const int64_t nev = n & ~int64_t(1);
-    // software pipeline: the loads of step s+1 are in flight while step s computes
+    // Software pipeline, ping-pong: the loads of step s+1 are in flight while step s
+    // computes; two named buffers (no register copies between iterations).
     const typename COST::Col cl0{};
-    typename COST::template Pre2<R> pre;
-    double2 bpre[K], sdpre = make_double2(0.0, 0.0);
+    typename COST::template Pre2<R> pa, pb;
+    double2 ba[K], bb[K], sda = make_double2(0.0, 0.0), sdb = make_double2(0.0, 0.0);
+    const int64_t stride = 2 * RP_THREADS;
     int64_t j = 2 * threadIdx.x;
-    if (j < nev) {
-      cost.pre2(rows, cl0, j, pre);
+    auto fetch = [&](int64_t jj, typename COST::template Pre2<R>& p, double2 (&bv)[K], double2& sdv) {
+      cost.pre2(rows, cl0, jj, p);
 #pragma unroll
-      for (int k = 0; k < K; ++k) bpre[k] = __ldg(reinterpret_cast<const double2*>(A.b[k] + j));
-      if (EVAL) sdpre = __ldg(reinterpret_cast<const double2*>(A.sd + j));
-    }
-    for (; j < nev; j += 2 * RP_THREADS) {
-      const typename COST::template Pre2<R> cur = pre;
-      double nb0[K], nb1[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) { nb0[k] = -bpre[k].x; nb1[k] = -bpre[k].y; }
-      const double2 sdv = sdpre;
-      const int64_t jn = j + 2 * RP_THREADS;
-      if (jn < nev) {
-        cost.pre2(rows, cl0, jn, pre);
-#pragma unroll
-        for (int k = 0; k < K; ++k) bpre[k] = __ldg(reinterpret_cast<const double2*>(A.b[k] + jn));
-        if (EVAL) sdpre = __ldg(reinterpret_cast<const double2*>(A.sd + jn));
-      }
+      for (int k = 0; k < K; ++k) bv[k] = __ldg(reinterpret_cast<const double2*>(A.b[k] + jj));
+      if (EVAL) sdv = __ldg(reinterpret_cast<const double2*>(A.sd + jj));
+    };
+    auto compute = [&](const typename COST::template Pre2<R>& p, const double2 (&bv)[K], const double2& sdv) {
       double cc[R][2];
-      cost.get2(rows, cl0, cur, cc);
+      cost.get2(rows, cl0, p, cc);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double c0 = cc[r][0], c1 = cc[r][1];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          double x0 = fma(na[k], c0, nb0[k]);
-          double x1 = fma(na[k], c1, nb1[k]);
+          const double x0 = fma(na[k], c0, -bv[k].x);
+          const double x1 = fma(na[k], c1, -bv[k].y);
           if (EVAL && k == 0) {
-            double e0 = texp(tab, x0, mlo[r][0], loff);
-            double e1 = texp(tab, x1, mlo[r][0], loff);
+            const double e0 = texp(tb, x0, mlo[r][0]);
+            const double e1 = texp(tb, x1, mlo[r][0]);
             acc[r][0] += e0 + e1;
             U[r] = fma(e0, c0, fma(e1, c1, U[r]));
             V[r] = fma(e0, x0, fma(e1, x1, V[r]));
             mn[r] = fmin(mn[r], fmin(c0 + sdv.x, c1 + sdv.y));
           } else {
-            texp_acc(tab, x0, mlo[r][k], loff, acc[r][k]);
-            texp_acc(tab, x1, mlo[r][k], loff, acc[r][k]);
+            texp_acc(tb, x0, mlo[r][k], acc[r][k]);
+            texp_acc(tb, x1, mlo[r][k], acc[r][k]);
           }
         }
       }
+    };
+    if (j < nev) fetch(j, pa, ba, sda);
+    // steady state: two steps per trip
+    for (; j + stride < nev; j += 2 * stride) {
+      fetch(j + stride, pb, bb, sdb);
+      compute(pa, ba, sda);
+      if (j + 2 * stride < nev) fetch(j + 2 * stride, pa, ba, sda);
+      compute(pb, bb, sdb);
     }
+    if (j < nev) compute(pa, ba, sda);
     if ((n & 1) && threadIdx.x == 0) {  // odd tail column
       const int64_t j = n - 1;
 #pragma unroll
@@ -144,7 +142,7 @@ __global__ void __launch_bounds__(RP_THREADS, 2) rowpass_kernel(const RowPassArg
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           double x0 = fma(na[k], c0, -__ldg(A.b[k] + j));
-          double e0 = texp(tab, x0, mlo[r][k], loff);
+          double e0 = texp(tb, x0, mlo[r][k]);
           acc[r][k] += e0;
           if (EVAL && k == 0) {
             U[r] = fma(e0, c0, U[r]);
@@ -202,8 +200,7 @@ __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
   if (cnt == 0) return;
   load_table(reinterpret_cast<double*>(smem));
   __syncthreads();
-  const char* tab = smem;
-  const uint32_t loff = lane_tab_off();
+  const uint32_t tb = lane_tab_addr(smem);
   const COST cost(A.cost);
   const int64_t n = A.cost.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -228,7 +225,7 @@ __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
     const uint32_t mlo = (uint32_t)m;
     double s = 0.0;
     for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
-      texp_acc(tab, fma(na, cost.eval1(row, j), -A.b[k][j]), mlo, loff, s);
+      texp_acc(tb, fma(na, cost.eval1(row, j), -A.b[k][j]), mlo, s);
     s = warp_sum(s);
     __syncthreads();
     if (lane == 0) red[warp] = s;
@@ -298,8 +295,7 @@ __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A
   uint32_t* s_m = reinterpret_cast<uint32_t*>(s_coef + CP_CHUNK * K * 4);  // [CP_CHUNK][K]
   load_table(reinterpret_cast<double*>(smem));
   __syncthreads();
-  const char* tab = smem;
-  const uint32_t loff = lane_tab_off();
+  const uint32_t tb = lane_tab_addr(smem);
   const COST cost(A.cost);
   const int64_t n = A.cost.n, nr = A.i1 - A.i0;
   const int64_t ntiles = (n + CP_TILE - 1) / CP_TILE;
@@ -341,18 +337,19 @@ __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A
       }
       __syncthreads();
       if (full) {
+        // 2-row ping-pong: rows (q, q+1) compute while rows (q+2, q+3) load
         typename COST::Row row = cost.row(q0);
-        typename COST::Pre4 pre;
-        cost.pre4(row, j, pre);
-        for (int q = 0; q < nq; ++q) {
-          const typename COST::Pre4 cur = pre;
-          if (q + 1 < nq) {
-            if constexpr (COST::kStored) row.p += cost.ld;
-            else row = cost.row(q0 + q + 1);
-            cost.pre4(row, j, pre);
+        typename COST::Pre4 pa0, pa1, pb0, pb1;
+        auto fetch = [&](typename COST::Pre4& p, int q) {
+          if (q < nq) {
+            if constexpr (COST::kStored) cost.pre4(row, j, p);
+            else cost.pre4(cost.row(q0 + q), j, p);
           }
+          if constexpr (COST::kStored) row.p += cost.ld;
+        };
+        auto compute = [&](const typename COST::Pre4& p, int q) {
           double c[CP_V];
-          cost.get4(cur, cl, c);
+          cost.get4(p, cl, c);
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             const double2 g01 = *reinterpret_cast<const double2*>(s_coef + (q * K + k) * 4);
@@ -360,9 +357,24 @@ __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A
             const uint32_t mlo = s_m[q * K + k];
 #pragma unroll
             for (int v = 0; v < CP_V; ++v)
-              texp_gacc(tab, fma(na[k], c[v], nb[k][v]), mlo, loff, g01.x, g01.y, g23.x, g23.y, acc[k][v]);
+              texp_gacc(tb, fma(na[k], c[v], nb[k][v]), mlo, g01.x, g01.y, g23.x, g23.y, acc[k][v]);
           }
+        };
+        fetch(pa0, 0);
+        fetch(pa1, 1);
+        int q = 0;
+        for (; q + 2 < nq; q += 4) {
+          fetch(pb0, q + 2);
+          fetch(pb1, q + 3);
+          compute(pa0, q);
+          compute(pa1, q + 1);
+          fetch(pa0, q + 4);
+          fetch(pa1, q + 5);
+          compute(pb0, q + 2);
+          if (q + 3 < nq) compute(pb1, q + 3);
         }
+        if (q < nq) compute(pa0, q);
+        if (q + 1 < nq) compute(pa1, q + 1);
       } else if (nv > 0) {
         for (int q = 0; q < nq; ++q) {
           const typename COST::Row row = cost.row(q0 + q);
@@ -373,7 +385,7 @@ __global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A
 #pragma unroll
               for (int k = 0; k < K; ++k) {
                 const double* cf = s_coef + (q * K + k) * 4;
-                texp_gacc(tab, fma(na[k], cv, nb[k][v]), s_m[q * K + k], loff, cf[0], cf[1], cf[2], cf[3],
+                texp_gacc(tb, fma(na[k], cv, nb[k][v]), s_m[q * K + k], cf[0], cf[1], cf[2], cf[3],
                           acc[k][v]);
               }
             }
@@ -412,8 +424,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowlse_kernel(const CostView cv, i
   __shared__ double bc;
   load_table(reinterpret_cast<double*>(smem));
   __syncthreads();
-  const char* tab = smem;
-  const uint32_t loff = lane_tab_off();
+  const uint32_t tb = lane_tab_addr(smem);
   const COST cost(cv);
   const int64_t n = cv.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -434,7 +445,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowlse_kernel(const CostView cv, i
     double s = 0.0;
     for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) {
       double y = (sgn * cost.eval1(row, j) + __ldg(v + j)) * scale - xm;
-      texp_acc(tab, fmax(y, -1000.0), 0u, loff, s);
+      texp_acc(tb, fmax(y, -1000.0), 0u, s);
     }
     s = warp_sum(s);
     __syncthreads();
