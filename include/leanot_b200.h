@@ -165,6 +165,42 @@ int leanot_graph_launch(void* graph_exec, void* stream);
 int leanot_graph_destroy(void* graph_exec);
 
 /* ---- barycenter (barycenter.py:78-151) --------------------------------- */
+/* Workspace of dxgb_solve / dxgb_step (barycenter.py:108-151, 227-277).  m marginals share a, s, t.
+ * Per-marginal n-vectors are stacked k-major with stride ns; per-row arrays with stride nr.
+ * nr = row1-row0 (= n: single-process). */
+typedef struct leanot_bary_plan {
+  leanot_cost_t cost;
+  leanot_params_t prm;
+  int64_t n, row0, row1;
+  int64_t ns;            /* stride of the per-marginal n-vectors (even, >= n: 16-byte aligned slices) */
+  int32_t m, splits, nblk_upd, _pad;
+  const double* w;       /* m   barycenter weights (normalized) */
+  const double* c;       /* m*n marginals */
+  const double* c_tilde; /* m*n c_k + alpha/n */
+  double* delta;         /* m*n */
+  double* b;             /* m*n */
+  double* b_bar;         /* m*n */
+  double* bprime;        /* m*n scratch */
+  double* sd;            /* m*n 2 sup tanh(delta/2) */
+  double* scal;          /* 8: a, a_bar, s, t */
+  int64_t* shift;        /* m*nr */
+  int64_t* mu;           /* m*2*nr shifts used */
+  double* S;             /* m*2*nr row sums */
+  double* L;             /* 2*m*nr row log-normalizers */
+  double* r;             /* 2*n  r_now | r_bar (implicit barycenters) */
+  double* coef;          /* m*2*nr*4 */
+  double* rowstat;       /* m*3*nr */
+  double* slab;          /* splits*2*n */
+  double* col;           /* m*2*n */
+  double* partial;       /* >= 2*max(nblk_upd, ceil(n/256)) */
+  double* scratch;       /* n */
+  double* evalbuf;       /* 128 */
+  int32_t* flags;        /* 2 + 4*nr */
+} leanot_bary_plan_t;
+int leanot_bary_prepare(const leanot_bary_plan_t* plan, double a, double s, double t, int init_shift, void* stream);
+int leanot_bary_sweep(const leanot_bary_plan_t* plan, int flags, void* stream);
+int leanot_bary_update(const leanot_bary_plan_t* plan, void* stream);
+int leanot_bary_eval(const leanot_bary_plan_t* plan, void* stream);
 /* r_i proportional to exp(sum_k w_k L_ki), k-sum in sorted order (barycenter.py:90-97) */
 int leanot_bary_rmap(const double* L, int m, int64_t n, const double* w, double* r, double* scratch, void* stream);
 

@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libleanot_b200.so"
+LIB_PATH = Path(os.environ.get("LEANOT_LIB", str(_HERE / "libleanot_b200.so")))
 
 LEANOT_OK = 0
 LEANOT_EINVAL = -1
@@ -42,6 +42,14 @@ class DxgPlanT(C.Structure):
         (name, C.c_void_p) for name in (
             "r", "c", "c_tilde", "delta", "b", "b_bar", "bprime", "sd", "scal", "shift", "m", "S",
             "coef", "rowstat", "slab", "col", "partial", "evalbuf", "flags")]
+
+
+class BaryPlanT(C.Structure):
+    _fields_ = [("cost", CostT), ("prm", ParamsT), ("n", C.c_int64), ("row0", C.c_int64), ("row1", C.c_int64),
+                ("ns", C.c_int64), ("m", C.c_int32), ("splits", C.c_int32), ("nblk_upd", C.c_int32), ("_pad", C.c_int32)] + [
+        (name, C.c_void_p) for name in (
+            "w", "c", "c_tilde", "delta", "b", "b_bar", "bprime", "sd", "scal", "shift", "mu", "S", "L", "r",
+            "coef", "rowstat", "slab", "col", "partial", "scratch", "evalbuf", "flags")]
 
 
 _lib = None
@@ -83,6 +91,10 @@ def lib():
         "leanot_graph_destroy": ([vp], C.c_int),
         "leanot_bary_rmap": ([vp, C.c_int, i64, vp, vp, vp, vp], C.c_int),
         "leanot_sync": ([vp], C.c_int),
+        "leanot_bary_prepare": ([C.POINTER(BaryPlanT), dbl, dbl, dbl, C.c_int, vp], C.c_int),
+        "leanot_bary_sweep": ([C.POINTER(BaryPlanT), C.c_int, vp], C.c_int),
+        "leanot_bary_update": ([C.POINTER(BaryPlanT), vp], C.c_int),
+        "leanot_bary_eval": ([C.POINTER(BaryPlanT), vp], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -99,7 +111,7 @@ EXPORTS = (
     "leanot_plan_stats", "leanot_row_min", "leanot_row_lse_affine", "leanot_dxg_prepare",
     "leanot_dxg_sweep", "leanot_dxg_update", "leanot_dxg_eval", "leanot_dxg_iterate",
     "leanot_graph_create", "leanot_graph_launch", "leanot_graph_destroy", "leanot_bary_rmap",
-    "leanot_sync",
+    "leanot_sync", "leanot_bary_prepare", "leanot_bary_sweep", "leanot_bary_update", "leanot_bary_eval",
 )
 
 

@@ -1,0 +1,307 @@
+"""DXG for entropic OT barycenters on B200 -- drop-in for leanot.barycenter.
+
+Same names, arguments and dataclasses as the reference
+(/root/reference/pkg/src/leanot/barycenter.py).  One iteration is one device
+sweep per marginal over both half-steps' weight sets, the sorted k-sum r-map and
+one column pass per marginal (libleanot_b200.so: leanot_bary_*); evaluation is
+folded into the next iteration's sweep like in dxg.solve.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core import CostKernel, Histogram, as_device_kernel, as_weights
+from .dxg import (DxgParams, LogOddsField, Termination, TrajectoryPoint, TransportLogWeights, _plan_stats,
+                  _to_dev, _ws, _wsets)
+
+__all__ = ["BarycenterState", "BarycenterSolution", "barycenter_marginal", "dxgb_step", "dxgb_solve",
+           "barycenter_objective"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class BarycenterState:
+    """barycenter.py:44-75."""
+
+    deltas: np.ndarray
+    bs: np.ndarray
+    a: float
+    s: float
+    t: int
+    w: np.ndarray
+    eta: float
+
+    @classmethod
+    def initial(cls, n: int, weights, eta: float) -> "BarycenterState":
+        if eta <= 0:
+            raise ValueError("barycenter solver requires eta > 0")
+        w = np.asarray(weights, dtype=float).ravel()
+        if np.any(w <= 0):
+            raise ValueError("weights must be positive")
+        w = w / w.sum()
+        m = w.size
+        return cls(np.zeros((m, n)), np.zeros((m, n)), 0.0, 0.0, 0, w, eta)
+
+    @property
+    def m(self) -> int:
+        return self.w.size
+
+    def weights_k(self, k: int) -> TransportLogWeights:
+        return TransportLogWeights(self.a, self.bs[k], self.s, self.t)
+
+    def mu_k(self, k: int) -> LogOddsField:
+        return LogOddsField(self.deltas[k])
+
+
+@dataclass
+class BarycenterSolution:
+    barycenter: Histogram
+    state: BarycenterState
+    converged: bool
+    iterations: int
+    seconds: float
+    trajectory: list[TrajectoryPoint]
+    per_marginal_infeas: np.ndarray = field(default=None)
+    workers: int = 1
+
+    @property
+    def final(self) -> TrajectoryPoint:
+        return self.trajectory[-1]
+
+
+class BaryEngine:
+    """Device state + workspaces of one barycenter solve (single process)."""
+
+    def __init__(self, kernel: CostKernel, marginals, w, params: DxgParams):
+        torch = _torch()
+        self.kernel = kernel
+        self.device = dev = kernel.device
+        n = self.n = kernel.n
+        M = np.stack([as_weights(h) for h in marginals])
+        m = self.m = M.shape[0]
+        if M.shape[1] != n:
+            raise ValueError("state/marginal/kernel size mismatch")
+        wv = np.asarray(w, dtype=float).ravel()
+        self.params = params
+        L = _lib.lib()
+        s = C.c_int(1)
+        L.leanot_dxg_default_splits(n, n, C.byref(s))
+        splits = s.value
+        sms = C.c_int(148)
+        L.leanot_device_sm_count(dev.index or 0, C.byref(sms))
+        nblk = int(min(max(1, (n + 255) // 256), 2 * sms.value))
+        f64 = dict(dtype=torch.float64, device=dev)
+        ns = self.ns = n + (-n) % 4                      # 16-byte aligned per-marginal slices
+        self.w = torch.from_numpy(wv).to(dev)
+        z = lambda *shape: torch.zeros(*shape, **f64)   # noqa: E731
+        self.c = z(m, ns)
+        self.c[:, :n] = torch.from_numpy(np.ascontiguousarray(M)).to(dev)
+        self.c_tilde = self.c + params.alpha / n          # c_k + alpha/n (barycenter.py:130)
+        self.delta, self.b, self.b_bar, self.bprime, self.sd = (z(m * ns) for _ in range(5))
+        self.scal = z(8)
+        self.shift = torch.zeros(m * n, dtype=torch.int64, device=dev)
+        self.mu = torch.zeros(2 * m * n, dtype=torch.int64, device=dev)
+        self.S = z(2 * m * n)
+        self.L = z(2 * m * n)
+        self.r = z(2 * n)
+        self.coef = z(8 * m * n)
+        self.rowstat = z(3 * m * n)
+        self.slab = z(splits * 2 * n)
+        self.col = z(2 * m * n)
+        self.partial = z(2 * max(nblk, (n + 255) // 256) + 2048)
+        self.scratch = z(n)
+        self.evalbuf = z(128)
+        self.flags = torch.zeros(2 + 4 * n, dtype=torch.int32, device=dev)
+        p = self.plan = _lib.BaryPlanT()
+        p.cost = kernel.cost_struct()
+        p.prm = _lib.ParamsT(params.eta, params.eta_mu, params.tau_p, params.tau_mu, params.beta, params.alpha)
+        p.n, p.row0, p.row1, p.ns, p.m, p.splits, p.nblk_upd = n, 0, n, ns, m, int(splits), nblk
+        for name in ("w", "c", "c_tilde", "delta", "b", "b_bar", "bprime", "sd", "scal", "shift", "mu", "S", "L",
+                     "r", "coef", "rowstat", "slab", "col", "partial", "scratch", "evalbuf", "flags"):
+            setattr(p, name, getattr(self, name).data_ptr())
+        self.M = M
+        self.wv = wv
+
+    def _call(self, name, *args):
+        with _torch().cuda.device(self.device):
+            _lib.check(getattr(_lib.lib(), name)(C.byref(self.plan), *args, _lib.stream_handle()), name)
+
+    def load_state(self, deltas, bs, a, s, t, fresh=False):
+        torch = _torch()
+        m, n, ns = self.m, self.n, self.ns
+        self.delta.view(m, ns)[:, :n].copy_(torch.as_tensor(np.ascontiguousarray(deltas, dtype=float)))
+        self.b.view(m, ns)[:, :n].copy_(torch.as_tensor(np.ascontiguousarray(bs, dtype=float)))
+        self._call("leanot_bary_prepare", float(a), float(s), float(t), 1 if fresh else 0)
+
+    def sweep(self, evaluate=False):
+        self._call("leanot_bary_sweep", 1 if evaluate else 0)
+
+    def update(self):
+        self._call("leanot_bary_update")
+
+    def read_state(self):
+        sc = self.scal[:4].cpu().tolist()
+        m, n, ns = self.m, self.n, self.ns
+        return (self.delta.view(m, ns)[:, :n].cpu().numpy(), self.b.view(m, ns)[:, :n].cpu().numpy(), sc[0], sc[2],
+                int(round(sc[3])))
+
+    def barycenter(self):
+        """r_now of the last sweep = barycenter_marginal(state) (barycenter.py:100-105)."""
+        return self.r[: self.n].cpu().numpy()
+
+    def evaluate(self):
+        """(primal, dual, infeas[m]) of the state swept by the last sweep(evaluate=True)."""
+        self._call("leanot_bary_eval")
+        buf = self.evalbuf.cpu().numpy()
+        eta, sup = self.params.eta, self.kernel.sup_norm
+        r = self.barycenter()
+        pos = r > 0
+        h_r = float(-(r[pos] * np.log(r[pos])).sum())
+        primal = 0.0
+        infeas = np.empty(self.m)
+        lead = 0.0
+        for k in range(self.m):
+            cost_k, ent_rows_k = buf[4 * k], buf[4 * k + 1]
+            infeas[k], cd_k = buf[64 + 2 * k], buf[64 + 2 * k + 1]
+            ent_k = ent_rows_k + h_r
+            primal += self.wv[k] * (cost_k + 2.0 * sup * infeas[k] - eta * ent_k)   # barycenter.py:222
+            lead += self.wv[k] * (-2.0 * sup * cd_k)                                # barycenter.py:192
+        dual = lead - eta * float(buf[127])                                         # barycenter.py:195
+        return primal, dual, infeas
+
+
+def _log_normalizers(a: float, bs: np.ndarray, kernel: CostKernel, workers: int = 1) -> np.ndarray:
+    """(m, n) LSE_j(-(a C_ij + b_kj)) (barycenter.py:78-87), one device sweep per marginal."""
+    torch = _torch()
+    dev = kernel.device
+    m, n = bs.shape
+    with torch.cuda.device(dev):
+        bt = [_to_dev(bs[k], dev) for k in range(m)]
+        w, keep = _wsets(dev, [(a, b) for b in bt])
+        out = torch.empty(m * n, dtype=torch.float64, device=dev)
+        ws = _ws(kernel, 1, n)
+        _lib.check(_lib.lib().leanot_row_lse(kernel.cost_struct(), 0, n, C.byref(w), out.data_ptr(), ws.data_ptr(),
+                                             _lib.stream_handle()), "row_lse")
+        res = out.view(m, n).cpu().numpy()
+        del keep
+    return res
+
+
+def _marginal_from_logz(w: np.ndarray, log_z: np.ndarray, device) -> Histogram:
+    """Sorted k-sum r-map on device (barycenter.py:90-97)."""
+    torch = _torch()
+    m, n = log_z.shape
+    with torch.cuda.device(device):
+        Lt = _to_dev(np.ascontiguousarray(log_z), device)
+        wt = _to_dev(w, device)
+        r = torch.empty(n, dtype=torch.float64, device=device)
+        scratch = torch.empty(n + 4096, dtype=torch.float64, device=device)
+        _lib.check(_lib.lib().leanot_bary_rmap(Lt.data_ptr(), m, n, wt.data_ptr(), r.data_ptr(), scratch.data_ptr(),
+                                               _lib.stream_handle()), "bary_rmap")
+        return Histogram(r.cpu().numpy())
+
+
+def barycenter_marginal(state: BarycenterState, kernel: CostKernel, workers: int = 1) -> Histogram:
+    """r_i proportional to exp(sum_k w_k log Z_ki) (barycenter.py:100-105)."""
+    if state.eta <= 0:
+        raise ValueError("barycenter map requires eta > 0")
+    kernel = as_device_kernel(kernel)
+    return _marginal_from_logz(state.w, _log_normalizers(state.a, state.bs, kernel, workers), kernel.device)
+
+
+def dxgb_step(state: BarycenterState, kernel: CostKernel, marginals, params: DxgParams,
+              workers: int = 1) -> BarycenterState:
+    """One extragradient iteration across all marginals (barycenter.py:108-151)."""
+    if params.eta <= 0:
+        raise ValueError("barycenter solver requires eta > 0")
+    m, n = state.deltas.shape
+    if len(marginals) != m or kernel.n != n:
+        raise ValueError("state/marginal/kernel size mismatch")
+    kernel = as_device_kernel(kernel)
+    eng = BaryEngine(kernel, marginals, state.w, params)
+    eng.load_state(state.deltas, state.bs, state.a, state.s, state.t, fresh=False)
+    eng.sweep()
+    eng.update()
+    deltas, bs, a, s, _ = eng.read_state()
+    return BarycenterState(deltas, bs, a, s, state.t + 1, state.w, state.eta)
+
+
+def barycenter_objective(state: BarycenterState, kernel: CostKernel, marginals, w=None, eta: float | None = None,
+                         workers: int = 1) -> float:
+    """sum_k w_k (<C, D_r p_k> + 2||C|| ||c(D_r p_k) - c_k||_1 - eta H(D_r p_k)) (barycenter.py:154-169)."""
+    weights = state.w if w is None else np.asarray(w, dtype=float) / np.sum(w)
+    eta_val = state.eta if eta is None else eta
+    kernel = as_device_kernel(kernel)
+    r = barycenter_marginal(state, kernel, workers)
+    total = 0.0
+    for k in range(len(marginals)):
+        cost, col, ent = _plan_stats(state.weights_k(k), kernel, r, workers)
+        pen = 2.0 * kernel.sup_norm * float(np.abs(col - as_weights(marginals[k])).sum())
+        total += weights[k] * (cost + pen - eta_val * ent)
+    return total
+
+
+def dxgb_solve(kernel: CostKernel, marginals, w, params: DxgParams, termination: Termination = Termination(),
+               log_stride: int = 25, workers: int = 1) -> BarycenterSolution:
+    """Iterate to gap and worst column infeasibility <= eps/6 (barycenter.py:227-277)."""
+    if params.eta <= 0:
+        raise ValueError("barycenter solver requires eta > 0")
+    kernel = as_device_kernel(kernel)
+    torch = _torch()
+    state0 = BarycenterState.initial(kernel.n, w, params.eta)
+    eng = BaryEngine(kernel, marginals, state0.w, params)
+    eng.load_state(state0.deltas, state0.bs, 0.0, 0.0, 0, fresh=True)
+    t0 = time.perf_counter()
+    trajectory: list[TrajectoryPoint] = []
+    converged = False
+    it = 0
+    swept = False
+    infeas = None
+
+    def log_point():
+        nonlocal swept, infeas
+        if not swept:
+            eng.sweep(evaluate=True)
+            swept = True
+        primal, dual, infeas = eng.evaluate()
+        s_val = float(eng.scal[2].item())
+        point = TrajectoryPoint(it, time.perf_counter() - t0, primal, dual, primal - dual, float(infeas.max()), s_val)
+        trajectory.append(point)
+        return point
+
+    while it < termination.max_iter:
+        if not swept:
+            eng.sweep()
+        eng.update()
+        swept = False
+        it += 1
+        timed_out = False
+        if termination.timeout is not None:
+            torch.cuda.synchronize(eng.device)
+            timed_out = time.perf_counter() - t0 > termination.timeout
+        if it % log_stride == 0 or it == termination.max_iter or timed_out:
+            eng.sweep(evaluate=True)
+            swept = True
+            point = log_point()
+            if point.gap <= termination.eps / 6.0 and point.col_infeas_l1 <= termination.eps / 6.0:
+                converged = True
+                break
+        if timed_out:
+            break
+    if not trajectory or trajectory[-1].iter != it:
+        log_point()
+    deltas, bs, a, s, _ = eng.read_state()
+    state = BarycenterState(deltas, bs, a, s, it, state0.w, params.eta)
+    return BarycenterSolution(barycenter=Histogram(eng.barycenter()), state=state, converged=converged,
+                              iterations=it, seconds=time.perf_counter() - t0, trajectory=trajectory,
+                              per_marginal_infeas=infeas, workers=workers)

@@ -2,3 +2,4 @@
 // and the template instantiations exist exactly once; no -rdc needed).
 #include "leanot_sweep.cu"
 #include "leanot_solver.cu"
+#include "leanot_bary.cu"

@@ -23,6 +23,15 @@
 
 namespace leanot {
 
+#ifndef LEANOT_RP_R
+#define LEANOT_RP_R 4     // rows per pass-A CTA step (K <= 2)
+#endif
+#ifndef LEANOT_RP_MINB
+#define LEANOT_RP_MINB 2  // pass-A CTAs per SM the register budget targets
+#endif
+#ifndef LEANOT_CP_MINB
+#define LEANOT_CP_MINB 2  // pass-B CTAs per SM the register budget targets
+#endif
 constexpr int RP_THREADS = 256;
 constexpr int CP_THREADS = 256;
 constexpr int CP_V = 4;                  // columns per thread in the column pass
@@ -52,7 +61,7 @@ __device__ __forceinline__ void finalize_row(const RowPassArgs& A, int k, int64_
 }
 
 template <class COST, int K, int R, bool EVAL>
-__global__ void __launch_bounds__(RP_THREADS, 2) rowpass_kernel(const RowPassArgs A) {
+__global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(const RowPassArgs A) {
   extern __shared__ __align__(16) char smem[];
   constexpr int NV = R * K + (EVAL ? 3 * R : 0);
   __shared__ double red[RP_THREADS / 32][NV];
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowmax_kernel(const RowPassArgs A,
 // cost); per-row constants (shift, g*EC0..3) are staged in shared memory and read
 // as broadcasts.
 template <class COST, int K>
-__global__ void __launch_bounds__(CP_THREADS) colpass_kernel(const ColPassArgs A) {
+__global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(const ColPassArgs A) {
   extern __shared__ __align__(16) char smem[];
   double* s_coef = reinterpret_cast<double*>(smem + TAB_BYTES);            // [CP_CHUNK][K][4]
   uint32_t* s_m = reinterpret_cast<uint32_t*>(s_coef + CP_CHUNK * K * 4);  // [CP_CHUNK][K]
@@ -551,8 +560,9 @@ struct RowPassFn {
   template <class COST>
   int run() {
     int rc;
-    if (K == 1) rc = eval ? launch_rowpass_t<COST, 1, 4, true>(A, st) : launch_rowpass_t<COST, 1, 4, false>(A, st);
-    else if (K == 2) rc = eval ? launch_rowpass_t<COST, 2, 4, true>(A, st) : launch_rowpass_t<COST, 2, 4, false>(A, st);
+    constexpr int R = LEANOT_RP_R;
+    if (K == 1) rc = eval ? launch_rowpass_t<COST, 1, R, true>(A, st) : launch_rowpass_t<COST, 1, R, false>(A, st);
+    else if (K == 2) rc = eval ? launch_rowpass_t<COST, 2, R, true>(A, st) : launch_rowpass_t<COST, 2, R, false>(A, st);
     else return LEANOT_EINVAL;
     if (rc != LEANOT_OK) return rc;
     if (A.flags) return launch_fixup_t<COST>(A, st);
