@@ -204,6 +204,36 @@ int leanot_bary_eval(const leanot_bary_plan_t* plan, void* stream);
 /* r_i proportional to exp(sum_k w_k L_ki), k-sum in sorted order (barycenter.py:90-97) */
 int leanot_bary_rmap(const double* L, int m, int64_t n, const double* w, double* r, double* scratch, void* stream);
 
+/* ---- Sinkhorn / IBP baselines (sinkhorn.py:47-228) -- */
+int64_t leanot_col_lse_ws_doubles(int64_t n, int64_t rows);
+/* L_j = LSE_i((phi_i - C_ij)/eta) over rows [row0,row1) (sinkhorn.py:47-62); row LSEs: leanot_row_lse_affine */
+int leanot_col_lse(const leanot_cost_t* cost, int64_t row0, int64_t row1, const double* phi, double eta, double* L,
+                   double* ws, void* stream);
+/* out = eta*log(w) - eta*L (potential update, sinkhorn.py:98) */
+int leanot_eta_log_minus(const double* w, const double* L, double eta, int64_t n, double* out, void* stream);
+/* psi_new = eta*log c - eta*L and gap = sum |c*expm1((psi - psi_new)/eta)| (sinkhorn.py:99-102) */
+int leanot_sinkhorn_psi(const double* c, const double* L, const double* psi, double eta, int64_t n, double* psi_new,
+                        double* gap, void* stream);
+/* <phi,r> + <psi,c> - eta*LSE_i(phi_i/eta + L_i), L = row LSE of (psi - C)/eta (sinkhorn.py:120-136) */
+int leanot_eot_dual(const double* phi, const double* psi, const double* r, const double* c, const double* L,
+                    double eta, int64_t n, double* out, void* stream);
+/* normalized column marginal of the plan, L = col LSE of (phi - C)/eta (sinkhorn.py:139-150) */
+int leanot_sinkhorn_colmarg(const double* psi, const double* L, double eta, int64_t n, double* col, void* stream);
+/* IBP shared-row step: log_r = sum_k w_k (phi_k/eta + RL_k); phi_k = eta*log_r - eta*RL_k (sinkhorn.py:222-224) */
+int leanot_ibp_rows(const double* w, int m, int64_t n, double eta, const double* RL, double* phis, double* log_r,
+                    void* stream);
+
+/* ---- dense post-processing, n <= dense cap ---------- */
+/* P_ij = r_i exp(-(a C_ij + b_j) - L_i), L from leanot_row_lse (materialize_plan, dxg.py:211-220) */
+int leanot_materialize_plan(const leanot_cost_t* cost, double a, const double* b, const double* r, const double* L,
+                            double* P, int64_t ld, void* stream);
+/* Alg. 1 Round onto Pi(r, c) in place (round_to_polytope, rounding.py:63-87); scratch >= 2n+2 doubles */
+int leanot_round_polytope(double* m, int64_t n, int64_t ld, const double* r, const double* c, double* scratch,
+                          void* stream);
+/* out[0] = <C, P> (rounded_cost, dxg.py:471); scratch >= 1024 doubles */
+int leanot_plan_cost(const leanot_cost_t* cost, const double* P, int64_t ld, double* out, double* scratch,
+                     void* stream);
+
 /* stream synchronize with error capture */
 int leanot_sync(void* stream);
 

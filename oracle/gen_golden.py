@@ -27,6 +27,7 @@ if REF not in sys.path:
 
 from leanot import barycenter as B  # noqa: E402
 from leanot import core, dxg  # noqa: E402
+from leanot import sinkhorn as SK  # noqa: E402
 
 OUT = Path(__file__).resolve().parents[1] / "tests" / "golden"
 
@@ -248,6 +249,42 @@ def gen_kat():
     save("kat_spec", meta=meta(), **kat)
 
 
+def gen_sinkhorn(rng):
+    """Sinkhorn / IBP baselines (sinkhorn.py:74-228) -- SURVEY.md §8f item 1."""
+    cases = {
+        "explicit_n37": core.ExplicitKernel(rng.random((37, 37))),
+        "grid_6x6_p2": core.GridKernel(6, 6, 2),
+        "points_n40_d3_p2": core.ColorKernel(rng.random((40, 3)), 2),
+    }
+    for name, k in cases.items():
+        n = k.n
+        r, c = rand_hist(rng, n), rand_hist(rng, n)
+        out = {"meta": meta(), "r": r.weights, "c": c.weights}
+        arr = kernel_arrays(name, k)
+        out["kind"] = np.asarray(arr.pop("kind"))
+        out.update({f"k_{kk}": np.asarray(v) for kk, v in arr.items()})
+        for eta, tol, mi in ((0.05, 1e-9, 10000), (0.01, 1e-8, 20000), (0.01, 1e-12, 7)):
+            pot = SK.sinkhorn_solve(k, r, c, eta, tol=tol, max_iter=mi)
+            tag = f"eta{eta}_mi{mi}"
+            out[f"{tag}_phi"], out[f"{tag}_psi"] = pot.phi, pot.psi
+            out[f"{tag}_info"] = np.array([pot.converged, pot.sweeps, pot.col_gap], dtype=float)
+            out[f"{tag}_dual"] = np.asarray(SK.eot_dual_value(pot, k, r, c))
+            out[f"{tag}_col"] = SK.sinkhorn_column_marginal(pot, k)
+        save(f"sinkhorn_{name}", **out)
+    g = core.GridKernel(5, 5, 2)
+    margs = [rand_hist(rng, 25) for _ in range(3)]
+    w = np.array([0.2, 0.5, 0.3])
+    out = {"meta": meta(), "margs": np.array([h.weights for h in margs]), "w": w}
+    for eta, tol, mi in ((0.05, 1e-9, 5000), (0.02, 1e-12, 9)):
+        res = SK.ibp_barycenter(g, margs, w, eta, tol=tol, max_iter=mi)
+        tag = f"eta{eta}_mi{mi}"
+        out[f"{tag}_bary"] = res.barycenter.weights
+        out[f"{tag}_phis"], out[f"{tag}_psis"] = res.phis, res.psis
+        out[f"{tag}_info"] = np.array([res.converged, res.sweeps, res.col_gap], dtype=float)
+        out[f"{tag}_logr"] = res.log_r
+    save("ibp_grid5x5_m3", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-config1", action="store_true")
@@ -258,6 +295,7 @@ def main():
     gen_steps(rng)
     gen_solves(rng)
     gen_bary(rng)
+    gen_sinkhorn(np.random.default_rng(777))
     if args.with_config1:
         gen_config1()
 

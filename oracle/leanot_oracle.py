@@ -538,3 +538,104 @@ def round_to_polytope(m, r, c):
 
 def default_workers():
     return max(1, len(os.sched_getaffinity(0)))
+
+
+# ---------------------------------------------------------------------------
+# Sinkhorn / IBP baselines (sinkhorn.py) -- SURVEY.md §8f item 1
+# ---------------------------------------------------------------------------
+
+
+def col_lse(cost, phi, eta, workers=1):
+    """_col_lse (sinkhorn.py:47-62): LSE_i((phi_i - C_ij)/eta), block-merged running max/sum."""
+    n = cost.n
+    run_m = np.full(n, -np.inf)
+    run_s = np.zeros(n)
+
+    def work(i0, i1):
+        z = (phi[i0:i1, None] - cost.block(i0, i1)) / eta
+        m = z.max(axis=0)
+        return m, np.exp(z - m[None, :]).sum(axis=0)
+
+    for m, s in run_blocks(work, n, workers):
+        new_m = np.maximum(run_m, m)
+        run_s = run_s * np.exp(run_m - new_m) + s * np.exp(m - new_m)
+        run_m = new_m
+    return run_m + np.log(run_s)
+
+
+def row_lse(cost, psi, eta, workers=1):
+    """_row_lse (sinkhorn.py:65-71): LSE_j((psi_j - C_ij)/eta)."""
+    return np.concatenate(run_blocks(lambda i0, i1: lse_rows((psi[None, :] - cost.block(i0, i1)) / eta),
+                                     cost.n, workers))
+
+
+def sinkhorn(cost, r, c, eta, tol=1e-9, max_iter=100_000, workers=1):
+    """sinkhorn_solve (sinkhorn.py:74-110) -> (phi, psi, converged, sweeps, col_gap), centered."""
+    log_r, log_c = np.log(r), np.log(c)
+    psi = np.zeros(cost.n)
+    best = None
+    for sweep in range(1, max_iter + 1):
+        phi = eta * log_r - eta * row_lse(cost, psi, eta, workers)
+        psi_new = eta * log_c - eta * col_lse(cost, phi, eta, workers)
+        gap = float(np.abs(c * np.expm1((psi - psi_new) / eta)).sum())
+        if best is None or gap < best[4]:
+            best = (phi, psi, True, sweep, gap)
+        if gap <= tol:
+            sh = phi.mean()
+            return phi - sh, psi + sh, True, sweep, gap
+        psi = psi_new
+    phi, psi, _, sweep, gap = best
+    sh = phi.mean()
+    return phi - sh, psi + sh, False, sweep, gap
+
+
+def eot_dual(phi, psi, eta, cost, r, c, workers=1):
+    """eot_dual_value (sinkhorn.py:120-136)."""
+    run_m, run_s = -np.inf, 0.0
+    for m, s in run_blocks(lambda i0, i1: _blk_lse(phi, psi, eta, cost, i0, i1), cost.n, workers):
+        new_m = max(run_m, m)
+        run_s = run_s * np.exp(run_m - new_m) + s * np.exp(m - new_m)
+        run_m = new_m
+    return float(phi @ r + psi @ c - eta * (run_m + np.log(run_s)))
+
+
+def _blk_lse(phi, psi, eta, cost, i0, i1):
+    z = (phi[i0:i1, None] + psi[None, :] - cost.block(i0, i1)) / eta
+    m = z.max()
+    return m, np.exp(z - m).sum()
+
+
+def sinkhorn_col(phi, psi, eta, cost, workers=1):
+    """sinkhorn_column_marginal (sinkhorn.py:139-150)."""
+    col = np.zeros(cost.n)
+    for part in run_blocks(lambda i0, i1: np.exp((phi[i0:i1, None] + psi[None, :] - cost.block(i0, i1)) / eta)
+                           .sum(axis=0), cost.n, workers):
+        col += part
+    return col / col.sum()
+
+
+def ibp(cost, margs, weights, eta, tol=1e-9, max_iter=10_000, workers=1):
+    """ibp_barycenter (sinkhorn.py:174-228) -> (bary, phis, psis, converged, sweeps, gap, log_r)."""
+    m, n = len(margs), cost.n
+    w = np.asarray(weights, dtype=float).ravel()
+    w = w / w.sum()
+    log_c = np.stack([np.log(h) for h in margs])
+    phis, psis = np.zeros((m, n)), np.zeros((m, n))
+    log_r = np.full(n, -np.log(n))
+    gap, converged, sweeps = np.inf, False, 0
+    for sweeps in range(1, max_iter + 1):
+        psis_new = np.empty_like(psis)
+        gaps = np.empty(m)
+        for k in range(m):
+            psis_new[k] = eta * log_c[k] - eta * col_lse(cost, phis[k], eta, workers)
+            gaps[k] = np.abs(np.exp(log_c[k]) * np.expm1((psis[k] - psis_new[k]) / eta)).sum()
+        gap = float(gaps.max())
+        if sweeps > 1 and gap <= tol:
+            converged = True
+            break
+        psis = psis_new
+        row_lses = np.stack([row_lse(cost, psis[k], eta, workers) for k in range(m)])
+        log_r = (w[:, None] * (phis / eta + row_lses)).sum(axis=0)
+        phis = eta * log_r[None, :] - eta * row_lses
+    bary = np.exp(log_r - log_r.max())
+    return bary / bary.sum(), phis, psis, converged, sweeps, gap, log_r

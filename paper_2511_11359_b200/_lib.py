@@ -95,6 +95,16 @@ def lib():
         "leanot_bary_sweep": ([C.POINTER(BaryPlanT), C.c_int, vp], C.c_int),
         "leanot_bary_update": ([C.POINTER(BaryPlanT), vp], C.c_int),
         "leanot_bary_eval": ([C.POINTER(BaryPlanT), vp], C.c_int),
+        "leanot_col_lse_ws_doubles": ([i64, i64], i64),
+        "leanot_col_lse": ([C.POINTER(CostT), i64, i64, vp, dbl, vp, vp, vp], C.c_int),
+        "leanot_eta_log_minus": ([vp, vp, dbl, i64, vp, vp], C.c_int),
+        "leanot_sinkhorn_psi": ([vp, vp, vp, dbl, i64, vp, vp, vp], C.c_int),
+        "leanot_eot_dual": ([vp, vp, vp, vp, vp, dbl, i64, vp, vp], C.c_int),
+        "leanot_sinkhorn_colmarg": ([vp, vp, dbl, i64, vp, vp], C.c_int),
+        "leanot_ibp_rows": ([vp, C.c_int, i64, dbl, vp, vp, vp, vp], C.c_int),
+        "leanot_materialize_plan": ([C.POINTER(CostT), dbl, vp, vp, vp, vp, i64, vp], C.c_int),
+        "leanot_round_polytope": ([vp, i64, i64, vp, vp, vp, vp], C.c_int),
+        "leanot_plan_cost": ([C.POINTER(CostT), vp, i64, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -112,6 +122,9 @@ EXPORTS = (
     "leanot_dxg_sweep", "leanot_dxg_update", "leanot_dxg_eval", "leanot_dxg_iterate",
     "leanot_graph_create", "leanot_graph_launch", "leanot_graph_destroy", "leanot_bary_rmap",
     "leanot_sync", "leanot_bary_prepare", "leanot_bary_sweep", "leanot_bary_update", "leanot_bary_eval",
+    "leanot_col_lse_ws_doubles", "leanot_col_lse", "leanot_eta_log_minus", "leanot_sinkhorn_psi", "leanot_eot_dual",
+    "leanot_sinkhorn_colmarg", "leanot_ibp_rows", "leanot_materialize_plan", "leanot_round_polytope",
+    "leanot_plan_cost",
 )
 
 

@@ -3,3 +3,5 @@
 #include "leanot_sweep.cu"
 #include "leanot_solver.cu"
 #include "leanot_bary.cu"
+#include "leanot_sinkhorn.cu"
+#include "leanot_dense.cu"

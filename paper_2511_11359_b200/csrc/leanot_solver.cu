@@ -159,6 +159,64 @@ __global__ void dxg_update2(const UpdArgs U, int advance_scalars) {
   }
 }
 
+// Small n (launch-bound): slab reduce + K3 + K4 + K5 in one CTA (same arithmetic, same order
+// of operations per element; maxima are order-independent).
+__global__ void __launch_bounds__(1024) dxg_update_small(const UpdArgs U, const double* slab, int splits,
+                                                         double* col) {
+  __shared__ double red[32];
+  __shared__ double bc;
+  const int64_t n = U.n;
+  auto bmax = [&](double v) -> double {
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+      bc = t;
+    }
+    __syncthreads();
+    const double r = bc;
+    __syncthreads();
+    return r;
+  };
+  double mx = -INFINITY;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double cn = 0.0, cb = 0.0;
+    for (int q = 0; q < splits; ++q) { cn += slab[(q * 2) * n + j]; cb += slab[(q * 2 + 1) * n + j]; }
+    col[j] = cn;
+    col[n + j] = cb;
+    const double cj = U.c[j], ctj = U.ct[j], dj = U.delta[j];
+    const double dbar = md_step(U.A, U.B, dj, cn, cj, ctj);
+    double dn = md_step(U.A, U.B, dj, cb, cj, ctj);
+    dn = fmin(fmax(dn, -U.beta), U.beta);
+    const double bp = __dadd_rn(__dmul_rn(U.decay, U.b[j]), __dmul_rn(U.G, tanh(__dmul_rn(0.5, dbar))));
+    U.delta[j] = dn;
+    U.bprime[j] = bp;
+    mx = fmax(mx, bp);
+  }
+  const double M = bmax(mx);
+  mx = -INFINITY;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double bn = __dsub_rn(U.bprime[j], M);
+    const double d = tanh(__dmul_rn(0.5, U.delta[j]));
+    const double bb = __dadd_rn(__dmul_rn(U.decay, bn), __dmul_rn(U.G, d));
+    U.b[j] = bn;
+    U.sd[j] = __dmul_rn(U.twosup, d);
+    U.bprime[j] = bb;
+    mx = fmax(mx, bb);
+  }
+  const double Mb = bmax(mx);
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) U.b_bar[j] = __dsub_rn(U.bprime[j], Mb);
+  if (threadIdx.x == 0) {
+    const double a = __dadd_rn(__dmul_rn(U.decay, U.scal[0]), U.tau_p);
+    U.scal[0] = a;
+    U.scal[1] = __dadd_rn(__dmul_rn(U.decay, a), U.tau_p);
+    U.scal[2] = __dadd_rn(__dmul_rn(U.decay, U.scal[2]), U.tau_p_eta);
+    U.scal[3] = U.scal[3] + 1.0;
+  }
+}
+
 // K5: b_bar = b_bar' - max b_bar'
 __global__ void dxg_update3(const UpdArgs U) {
   const double M = max_of(U.partial + U.nblk, U.nblk);
@@ -375,6 +433,12 @@ static UpdArgs make_upd(const leanot_dxg_plan_t& P) {
   U.tau_p_eta = q.tau_p * q.eta;
   U.nblk = P.nblk_upd;
   return U;
+}
+
+// plans whose O(n) work fits one CTA and whose sweep covers all rows (single process):
+// launch-bound regime, fused update path
+static bool small_plan(const leanot_dxg_plan_t& P) {
+  return P.n <= 16384 && P.row0 == 0 && P.row1 == P.n;
 }
 
 static RowPassArgs make_rowpass(const leanot_dxg_plan_t& P) {
@@ -682,7 +746,9 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
   B.b[0] = P->b; B.b[1] = P->b_bar;
   B.m = P->m; B.coef = P->coef; B.slab = P->slab; B.splits = P->splits;
   LEANOT_TRY(launch_colpass(B, 2, st));
-  LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, P->n, P->col, st));
+  // small single-process plans fold the slab reduce into dxg_update_small, except on
+  // evaluation sweeps whose column marginal is read before the update
+  if (!small_plan(*P) || (flags & LEANOT_SWEEP_EVAL)) LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, P->n, P->col, st));
   return check_launch("dxg_sweep");
 }
 
@@ -690,6 +756,11 @@ int leanot_dxg_update(const leanot_dxg_plan_t* P, void* stream) {
   LEANOT_TRY(validate_plan(P));
   cudaStream_t st = S_(stream);
   UpdArgs U = make_upd(*P);
+  if (small_plan(*P)) {
+    // slabs -> col (again, if an eval sweep already reduced them: same values) + all O(n) updates
+    dxg_update_small<<<1, 1024, 0, st>>>(U, P->slab, P->splits, P->col);
+    return check_launch("dxg_update_small");
+  }
   dxg_update1<<<P->nblk_upd, 256, 0, st>>>(U);
   dxg_update2<<<P->nblk_upd, 256, 0, st>>>(U, 1);
   dxg_update3<<<P->nblk_upd, 256, 0, st>>>(U);

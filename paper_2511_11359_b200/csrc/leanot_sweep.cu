@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 
 #include "leanot_cost.cuh"
 #include "leanot_internal.h"
@@ -504,6 +506,33 @@ __global__ void cost_block_kernel(const CostView cv, int64_t i0, int64_t i1, dou
   }
 }
 
+// LEANOT_TMA=0 disables the TMA-staged stored-cost kernels (A/B comparisons)
+static bool tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LEANOT_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static bool tma_cols_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LEANOT_TMA_COLS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+int num_sms();
+
+}  // namespace leanot
+
+#include "leanot_sweep_tma.cu"
+
+namespace leanot {
+
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
@@ -561,6 +590,15 @@ struct RowPassFn {
   int run() {
     int rc;
     constexpr int R = LEANOT_RP_R;
+    if constexpr (std::is_same<COST, CostStored>::value) {
+      if (tma_ok(A.cost) && (K == 1 || K == 2)) {
+        if (K == 1) rc = eval ? launch_rowpass_tma_t<1, 4, true>(A, st) : launch_rowpass_tma_t<1, 4, false>(A, st);
+        else rc = eval ? launch_rowpass_tma_t<2, 4, true>(A, st) : launch_rowpass_tma_t<2, 4, false>(A, st);
+        if (rc != LEANOT_OK) return rc;
+        if (A.flags) return launch_fixup_t<COST>(A, st);
+        return LEANOT_OK;
+      }
+    }
     if (K == 1) rc = eval ? launch_rowpass_t<COST, 1, R, true>(A, st) : launch_rowpass_t<COST, 1, R, false>(A, st);
     else if (K == 2) rc = eval ? launch_rowpass_t<COST, 2, R, true>(A, st) : launch_rowpass_t<COST, 2, R, false>(A, st);
     else return LEANOT_EINVAL;
@@ -624,6 +662,14 @@ struct ColPassFn {
   cudaStream_t st;
   template <class COST>
   int run() {
+    if constexpr (std::is_same<COST, CostStored>::value) {
+      // the TMA column pass is kept for experiments (LEANOT_TMA_COLS=1); measured slower
+      // than the register-pipelined one (profiles/r01_tma.md)
+      if (tma_ok(A.cost) && tma_cols_enabled()) {
+        if (K == 1) return launch_colpass_tma_t<1>(A, st);
+        if (K == 2) return launch_colpass_tma_t<2>(A, st);
+      }
+    }
     if (K == 1) return launch_colpass_t<COST, 1>(A, st);
     if (K == 2) return launch_colpass_t<COST, 2>(A, st);
     return LEANOT_EINVAL;

@@ -24,7 +24,7 @@ import numpy as np
 from . import _lib
 from .core import DENSE_CAP, CostKernel, Histogram, as_device_kernel, as_weights
 from .engine import DxgEngine, default_group
-from .rounding import DenseCoupling, InfeasibilityReport, infeasibility, round_to_polytope
+from .rounding import DenseCoupling, InfeasibilityReport, infeasibility, round_on_device, round_to_polytope
 from .sinkhorn import DualPotentials
 
 __all__ = [
@@ -244,19 +244,34 @@ def column_marginal(state: TransportLogWeights, kernel: CostKernel, r: Histogram
     return _column_marginals(kernel, as_weights(r), [(state.a, state.b)])[0]
 
 
+def _plan_on_device(state: TransportLogWeights, kernel: CostKernel, r_w):
+    """D_r p as a device n x n tensor: row LSEs (sweep kernels) + one plan kernel."""
+    torch = _torch()
+    dev = kernel.device
+    n = kernel.n
+    with torch.cuda.device(dev):
+        bt = _to_dev(state.b, dev)
+        w, keep = _wsets(dev, [(state.a, bt)])
+        L = torch.empty(n, dtype=torch.float64, device=dev)
+        ws = _ws(kernel, 1, n)
+        lib = _lib.lib()
+        s = _lib.stream_handle()
+        _lib.check(lib.leanot_row_lse(kernel.cost_struct(), 0, n, C.byref(w), L.data_ptr(), ws.data_ptr(), s),
+                   "row_lse")
+        P = torch.empty((n, n), dtype=torch.float64, device=dev)
+        rt = _to_dev(r_w, dev)
+        _lib.check(lib.leanot_materialize_plan(kernel.cost_struct(), float(state.a), bt.data_ptr(), rt.data_ptr(),
+                                               L.data_ptr(), P.data_ptr(), n, s), "materialize_plan")
+        del keep
+    return P
+
+
 def materialize_plan(state: TransportLogWeights, kernel: CostKernel, r: Histogram, cap: int = DENSE_CAP) -> np.ndarray:
-    """Dense D_r p (dxg.py:211-220) on device, returned on the host."""
+    """Dense D_r p for rounding and tests (dxg.py:211-220), computed on device."""
     kernel = _dev_kernel(kernel)
     if kernel.n > cap:
         raise ValueError("implicit plan materialization above the dense cap")
-    torch = _torch()
-    dev = kernel.device
-    Cm = torch.from_numpy(kernel.materialize(cap)).to(dev)
-    z = -(state.a * Cm + _to_dev(state.b, dev)[None, :])
-    z -= z.max(dim=1, keepdim=True).values
-    e = torch.exp(z)
-    p = e / e.sum(dim=1, keepdim=True)
-    return (_to_dev(as_weights(r), dev)[:, None] * p).cpu().numpy()
+    return _plan_on_device(state, kernel, as_weights(r)).cpu().numpy()
 
 
 def dual_md_step(mu: LogOddsField, col_marginal, c: Histogram, c_tilde, params: DxgParams,
@@ -489,10 +504,14 @@ def solve(kernel: CostKernel, r: Histogram, c: Histogram, params: DxgParams,
     state = DxgState(LogOddsField(delta), TransportLogWeights(a=a, b=b, s=s, t=it))
     sol = DxgSolution(state, converged, it, seconds, trajectory, report, workers=workers)
     if kernel.n <= dense_cap:
-        plan = DenseCoupling(materialize_plan(state.weights, kernel, rw, dense_cap))
-        rounded = round_to_polytope(plan, rw, cw)
-        sol.rounded_plan = rounded
-        sol.rounded_cost = float((rounded.entries * kernel.materialize(dense_cap)).sum())
+        # materialize, Round (Alg. 1) and <C, pi> all on device (dxg.py:467-471)
+        P = round_on_device(_plan_on_device(state.weights, kernel, rw), rw, cw)
+        out = torch.empty(1025, dtype=torch.float64, device=kernel.device)
+        with torch.cuda.device(kernel.device):
+            _lib.check(_lib.lib().leanot_plan_cost(kernel.cost_struct(), P.data_ptr(), kernel.n, out[1024:].data_ptr(),
+                                                   out.data_ptr(), _lib.stream_handle()), "plan_cost")
+        sol.rounded_plan = DenseCoupling(P.cpu().numpy())
+        sol.rounded_cost = float(out[1024].item())
     return sol
 
 

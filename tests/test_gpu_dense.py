@@ -1,0 +1,73 @@
+"""Dense post-processing on the GPU: plan materialization and Alg. 1 Round."""
+
+import numpy as np
+import pytest
+
+import leanot_oracle as O
+from helpers import load, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def test_round_guarantee_random_trials():
+    """SPEC acceptance criterion 2 (Lemma 1): feasible to 1e-12, ||pi - pi~||_1 <= 2 (row_gap + col_gap)."""
+    from paper_2511_11359_b200.rounding import DenseCoupling, round_to_polytope
+    rng = np.random.default_rng(2)
+    for trial in range(120):
+        n = int(rng.integers(2, 33))
+        pi = rng.random((n, n)) * rng.random() / n
+        r = O.normalized_hist(rng.random(n) + 0.01)
+        c = O.normalized_hist(rng.random(n) + 0.01)
+        out = round_to_polytope(DenseCoupling(pi), r, c).entries
+        assert np.all(out >= 0)
+        assert np.abs(out.sum(axis=1) - r).sum() <= 1e-12
+        assert np.abs(out.sum(axis=0) - c).sum() <= 1e-12
+        gap = np.abs(pi.sum(axis=1) - r).sum() + np.abs(pi.sum(axis=0) - c).sum()
+        assert np.abs(pi - out).sum() <= 2 * gap + 1e-12
+        ref = O.round_to_polytope(pi, r, c)
+        if np.all(ref >= 0):
+            assert rel_err(out, ref) <= 1e-12
+
+
+def test_round_spec_example():
+    """SPEC.md rounding example: pi=[[0.6,0.2],[0.1,0.1]], r=c=(0.5,0.5) -> [[0.375,0.125],[0.125,0.375]]."""
+    from paper_2511_11359_b200.rounding import DenseCoupling, round_to_polytope
+    out = round_to_polytope(DenseCoupling(np.array([[0.6, 0.2], [0.1, 0.1]])), np.array([0.5, 0.5]),
+                            np.array([0.5, 0.5])).entries
+    assert np.allclose(out, [[0.375, 0.125], [0.125, 0.375]], atol=1e-15)
+
+
+def test_materialize_plan_matches_dense_reference():
+    from paper_2511_11359_b200 import core, dxg
+    d = load("sweep_explicit_n37")
+    k = core.ExplicitKernel(d["k_C"])
+    w = dxg.TransportLogWeights(float(d["case2_a"]), d["case2_b"], 0.0, 0)
+    P = dxg.materialize_plan(w, k, d["r"])
+    Cn = d["k_C"] / d["k_C"].max()
+    z = -(w.a * Cn + w.b[None, :])
+    z -= z.max(axis=1, keepdims=True)
+    e = np.exp(z)
+    ref = d["r"][:, None] * e / e.sum(axis=1, keepdims=True)
+    assert rel_err(P, ref) <= 1e-13
+    assert rel_err(P.sum(axis=0), d["case2_col"]) <= 1e-13
+
+
+def test_solve_with_rounding_is_feasible():
+    """dense_cap path of solve (dxg.py:467-471): rounded plan in Pi(r, c), cost = <C, plan>."""
+    from paper_2511_11359_b200 import core, dxg
+    d = load("solve_explicit_n64_taumu005")
+    k = core.ExplicitKernel(d["k_C"])
+    prm = dxg.DxgParams(*[float(v) for v in d["params"]])
+    sol = dxg.solve(k, d["r"], d["c"], prm, dxg.Termination(eps=float(d["term"][0]), max_iter=int(d["term"][1])))
+    assert sol.iterations == int(d["iterations"])
+    P = sol.rounded_plan.entries
+    assert np.all(P >= 0)
+    assert np.abs(P.sum(axis=1) - d["r"]).sum() <= 1e-12
+    assert np.abs(P.sum(axis=0) - d["c"]).sum() <= 1e-12
+    Cn = d["k_C"] / d["k_C"].max()
+    assert abs(sol.rounded_cost - float((P * Cn).sum())) <= 1e-13
+    # the oracle's Round of the same final plan (clamped deficits) agrees
+    w = sol.state.weights
+    plan = dxg.materialize_plan(w, k, d["r"])
+    assert rel_err(P, O.round_to_polytope(plan, d["r"], d["c"]) if np.all(
+        O.round_to_polytope(plan, d["r"], d["c"]) >= 0) else P) <= 1e-12

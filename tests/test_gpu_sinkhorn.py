@@ -1,0 +1,54 @@
+"""Sinkhorn / IBP baselines on the GPU vs the reference's golden vectors (sinkhorn.py)."""
+
+import numpy as np
+import pytest
+
+from helpers import device_cost, golden_names, load, rel_err
+
+pytestmark = pytest.mark.gpu
+
+SINKHORN = golden_names("sinkhorn_")
+
+
+@pytest.mark.parametrize("name", SINKHORN)
+def test_sinkhorn_vs_reference(name):
+    from paper_2511_11359_b200 import sinkhorn as SK
+    d = load(name)
+    k = device_cost(d)
+    r, c = d["r"], d["c"]
+    for eta, tol, mi in ((0.05, 1e-9, 10000), (0.01, 1e-8, 20000), (0.01, 1e-12, 7)):
+        tag = f"eta{eta}_mi{mi}"
+        pot = SK.sinkhorn_solve(k, r, c, eta, tol=tol, max_iter=mi)
+        info = d[f"{tag}_info"]
+        assert pot.converged == bool(info[0]) and pot.sweeps == int(info[1]), tag
+        assert abs(pot.col_gap - info[2]) <= 1e-11 + 1e-6 * info[2]
+        assert rel_err(pot.phi, d[f"{tag}_phi"]) <= 1e-10 and rel_err(pot.psi, d[f"{tag}_psi"]) <= 1e-10
+        assert abs(SK.eot_dual_value(pot, k, r, c) - float(d[f"{tag}_dual"])) <= 1e-11
+        assert rel_err(SK.sinkhorn_column_marginal(pot, k), d[f"{tag}_col"]) <= 1e-10
+
+
+def test_ibp_vs_reference():
+    from paper_2511_11359_b200 import core
+    from paper_2511_11359_b200 import sinkhorn as SK
+    d = load("ibp_grid5x5_m3")
+    g = core.GridKernel(5, 5, 2)
+    margs = [core.Histogram(h) for h in d["margs"]]
+    for eta, tol, mi in ((0.05, 1e-9, 5000), (0.02, 1e-12, 9)):
+        tag = f"eta{eta}_mi{mi}"
+        res = SK.ibp_barycenter(g, margs, d["w"], eta, tol=tol, max_iter=mi)
+        info = d[f"{tag}_info"]
+        assert res.converged == bool(info[0]) and res.sweeps == int(info[1])
+        assert rel_err(res.barycenter.weights, d[f"{tag}_bary"]) <= 1e-10
+        assert rel_err(res.phis, d[f"{tag}_phis"]) <= 1e-10 and rel_err(res.psis, d[f"{tag}_psis"]) <= 1e-10
+
+
+def test_sinkhorn_errors_like_reference():
+    from paper_2511_11359_b200 import core
+    from paper_2511_11359_b200 import sinkhorn as SK
+    k = core.GridKernel(3, 3, 1)
+    with pytest.raises(ValueError):
+        SK.sinkhorn_solve(k, np.full(9, 1 / 9), np.full(9, 1 / 9), 0.0)
+    r = np.full(9, 1 / 8)
+    r[0] = 0.0
+    with pytest.raises(ValueError):
+        SK.sinkhorn_solve(k, r, np.full(9, 1 / 9), 0.1)

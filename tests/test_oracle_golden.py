@@ -122,3 +122,34 @@ def test_hash_generator_properties():
     assert 0.0 <= blk.min() < 0.01
     assert np.array_equal(hc.block(128, 200), blk[128:200])   # regenerable block by block
     assert not np.array_equal(O.HashCost(300, seed=8).block(1, 2), blk[1:2])
+
+
+SINKHORN = golden_names("sinkhorn_")
+
+
+@pytest.mark.parametrize("name", SINKHORN)
+def test_sinkhorn_oracle_matches_reference(name):
+    d = load(name)
+    cost = oracle_cost(d)
+    r, c = d["r"], d["c"]
+    for eta, tol, mi in ((0.05, 1e-9, 10000), (0.01, 1e-8, 20000), (0.01, 1e-12, 7)):
+        tag = f"eta{eta}_mi{mi}"
+        phi, psi, conv, sweeps, gap = O.sinkhorn(cost, r, c, eta, tol=tol, max_iter=mi)
+        info = d[f"{tag}_info"]
+        assert conv == bool(info[0]) and sweeps == int(info[1])
+        assert abs(gap - info[2]) <= 1e-12 + 1e-9 * info[2]
+        assert rel_err(phi, d[f"{tag}_phi"]) <= 1e-12 and rel_err(psi, d[f"{tag}_psi"]) <= 1e-12
+        assert abs(O.eot_dual(phi, psi, eta, cost, r, c) - float(d[f"{tag}_dual"])) <= 1e-12
+        assert rel_err(O.sinkhorn_col(phi, psi, eta, cost), d[f"{tag}_col"]) <= 1e-12
+
+
+def test_ibp_oracle_matches_reference():
+    d = load("ibp_grid5x5_m3")
+    g = O.GridCost(5, 5, 2)
+    for eta, tol, mi in ((0.05, 1e-9, 5000), (0.02, 1e-12, 9)):
+        tag = f"eta{eta}_mi{mi}"
+        bary, phis, psis, conv, sweeps, gap, log_r = O.ibp(g, list(d["margs"]), d["w"], eta, tol=tol, max_iter=mi)
+        info = d[f"{tag}_info"]
+        assert conv == bool(info[0]) and sweeps == int(info[1])
+        assert rel_err(bary, d[f"{tag}_bary"]) <= 1e-12
+        assert rel_err(phis, d[f"{tag}_phis"]) <= 1e-12 and rel_err(psis, d[f"{tag}_psis"]) <= 1e-12

@@ -38,6 +38,9 @@ eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
 for _ in range(3):
     eng.sweep(); eng.update()
 torch.cuda.synchronize()
+import subprocess  # noqa: E402
+smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits",
+                        "-lms", "100"], stdout=subprocess.PIPE, text=True)
 st = torch.cuda.current_stream()
 ta, tb = [], []
 for _ in range(a.iters):
@@ -46,5 +49,7 @@ for _ in range(a.iters):
     eng.update()
     torch.cuda.synchronize()
     ta.append(e[0].elapsed_time(e[1])); tb.append(e[1].elapsed_time(e[2]))
+smi.terminate()
+clk = [float(line.split(",")[0]) for line in smi.stdout.read().splitlines() if line.strip()]
 print(json.dumps({"tag": a.tag, "n": n, "kind": a.kind, "rowpass_ms": statistics.median(ta),
-                  "colpass_ms": statistics.median(tb)}))
+                  "colpass_ms": statistics.median(tb), "sm_mhz": statistics.median(clk) if clk else None}))
