@@ -5,9 +5,9 @@
 // (cp.async.bulk ... mbarrier::complete_tx) issued by a dedicated producer warp, so
 // the 16 consumer warps never wait on HBM latency and hold no prefetch registers.
 //   pass A: stage = R rows x 960 columns of C + 960 columns of b and b_bar (45 KB), 3 stages
-//   pass B: stage = 1 row x 3840 columns of C (30 KB), 4 stages; 8 columns per thread
-// Ring protocol: full[s] (1 producer arrival + tx bytes) / empty[s] (512 consumer
-// arrivals); phase parity = (step / NS) & 1.
+//   pass B: stage = 2 rows x 1920 columns of C (30 KB), 4 stages; 4 columns per thread
+// Ring protocol: full[s] (1 producer arrival + tx bytes) / empty[s] (one arrival per
+// consumer warp); phase parity = (step / NS) & 1.
 // Included by leanot_lib.cu (single translation unit).
 
 namespace leanot {
@@ -42,6 +42,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// a warp releases a stage once all its lanes are done reading it (one arrival per warp)
+__device__ __forceinline__ void release(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(TP_THREADS) : "memory"); }
 
 template <int K, int R, bool EVAL>
@@ -58,7 +63,7 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
   double* red = reinterpret_cast<double*>(empty + NS);  // [NW][NV]
   load_table(reinterpret_cast<double*>(smem));
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, TP_THREADS); }
+    for (int s = 0; s < NS; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, TP_THREADS / 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
           }
         }
       }
-      mbar_arrive(empty + s);
+      release(empty + s);
     }
     // block reduction over the consumer warps, fixed order
 #pragma unroll
@@ -186,16 +191,17 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
   }
 }
 
-// pass B, stored cost: 3840-column tiles x row splits, 1 row per stage, 8 columns per
-// thread as 4 column pairs at 2t + p*960 (conflict-free 16-byte shared loads)
+// pass B, stored cost: 1920-column tiles x row splits, Q=2 rows per stage, 4 columns per
+// thread as 2 column pairs at 2t and 2t + 960 (conflict-free 16-byte shared loads)
 template <int K>
 __global__ void __launch_bounds__(TP_ALL, 1) colpass_tma_kernel(const ColPassArgs A) {
-  constexpr int V = 8;
-  constexpr int TILE = V * TP_THREADS;  // 3840
-  constexpr int PS = TILE / 4;          // pair stride
+  constexpr int V = 4;
+  constexpr int TILE = V * TP_THREADS;  // 1920
+  constexpr int PS = TILE / 2;          // pair stride
+  constexpr int Q = 2;                  // rows per stage
   constexpr int NS = 4;
-  constexpr int STAGE = TILE * 8;       // 30 KB
-  constexpr int CHUNK = 128;            // rows of per-row constants staged at once
+  constexpr int STAGE = Q * TILE * 8;   // 30 KB
+  constexpr int CHUNK = 128;            // rows of per-row constants staged at once (CHUNK % Q == 0)
   extern __shared__ __align__(128) char smem[];
   char* stages = smem + TAB_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + NS * STAGE);
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(TP_ALL, 1) colpass_tma_kernel(const ColPassArg
   uint32_t* s_m = reinterpret_cast<uint32_t*>(s_coef + CHUNK * K * 4);  // [CHUNK][K]
   load_table(reinterpret_cast<double*>(smem));
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, TP_THREADS); }
+    for (int s = 0; s < NS; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, TP_THREADS / 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -223,11 +229,17 @@ __global__ void __launch_bounds__(TP_ALL, 1) colpass_tma_kernel(const ColPassArg
         const uint32_t w = (uint32_t)((n - j0 < TILE ? n - j0 : TILE) * 8);
         const int64_t rs0 = A.i0 + split * rps;
         const int64_t rs1 = A.i1 < rs0 + rps ? A.i1 : rs0 + rps;
-        for (int64_t i = rs0; i < rs1; ++i, ++q) {
-          const int s = q % NS;
-          mbar_wait(empty + s, ((q / NS) & 1) ^ 1);
-          mbar_arrive_tx(full + s, w);
-          bulk_g2s(stages + s * STAGE, cv.mat + (i - cv.row_base) * cv.ld + j0, w, full + s);
+        // stage boundaries follow the consumers' chunks: CHUNK rows, Q rows per stage
+        for (int64_t c0 = rs0; c0 < rs1; c0 += CHUNK) {
+          const int64_t c1 = rs1 < c0 + CHUNK ? rs1 : c0 + CHUNK;
+          for (int64_t r0 = c0; r0 < c1; r0 += Q, ++q) {
+            const int s = q % NS;
+            mbar_wait(empty + s, ((q / NS) & 1) ^ 1);
+            const int nq = (int)(c1 - r0 < Q ? c1 - r0 : Q);
+            mbar_arrive_tx(full + s, nq * w);
+            for (int r = 0; r < nq; ++r)
+              bulk_g2s(stages + s * STAGE + r * TILE * 8, cv.mat + (r0 + r - cv.row_base) * cv.ld + j0, w, full + s);
+          }
         }
       }
     }
@@ -243,8 +255,8 @@ __global__ void __launch_bounds__(TP_ALL, 1) colpass_tma_kernel(const ColPassArg
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t tile = it % ntiles, split = it / ntiles;
     const int64_t nloc = n - tile * TILE;  // valid columns of this tile
-    const int l0 = 2 * (int)threadIdx.x;   // local offset of pair 0
-    const bool all_ok = l0 + 3 * PS + 1 < nloc;
+    const int l0 = 2 * (int)threadIdx.x;
+    const bool all_ok = l0 + PS + 1 < nloc;
     double nb[K][V], acc[K][V];
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -268,43 +280,51 @@ __global__ void __launch_bounds__(TP_ALL, 1) colpass_tma_kernel(const ColPassArg
         s_m[t] = (uint32_t)A.m[k * nr + (c0 - A.i0 + qq)];
       }
       consumer_sync();
-      for (int qq = 0; qq < nc; ++qq, ++q) {
+      for (int base = 0; base < nc; base += Q, ++q) {
         const int s = q % NS;
         mbar_wait(full + s, (q / NS) & 1);
-        const char* rowp = stages + s * STAGE + 16 * threadIdx.x;
-        if (all_ok) {
-          double c[V];
+        const int nq = nc - base < Q ? nc - base : Q;
+        if (all_ok && nq == Q) {
+          double c[Q][V];
 #pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            const double2 cc = *reinterpret_cast<const double2*>(rowp + p * PS * 8);
-            c[2 * p] = cc.x;
-            c[2 * p + 1] = cc.y;
+          for (int r = 0; r < Q; ++r) {
+            const char* rowp = stages + s * STAGE + r * TILE * 8 + 16 * threadIdx.x;
+            const double2 ca = *reinterpret_cast<const double2*>(rowp);
+            const double2 cb = *reinterpret_cast<const double2*>(rowp + PS * 8);
+            c[r][0] = ca.x; c[r][1] = ca.y; c[r][2] = cb.x; c[r][3] = cb.y;
           }
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const double2 g01 = *reinterpret_cast<const double2*>(s_coef + (qq * K + k) * 4);
-            const double2 g23 = *reinterpret_cast<const double2*>(s_coef + (qq * K + k) * 4 + 2);
-            const uint32_t mlo = s_m[qq * K + k];
+          for (int r = 0; r < Q; ++r) {
+            const int qq = base + r;
 #pragma unroll
-            for (int v = 0; v < V; ++v)
-              texp_gacc(tb, fma(na[k], c[v], nb[k][v]), mlo, g01.x, g01.y, g23.x, g23.y, acc[k][v]);
+            for (int k = 0; k < K; ++k) {
+              const double2 g01 = *reinterpret_cast<const double2*>(s_coef + (qq * K + k) * 4);
+              const double2 g23 = *reinterpret_cast<const double2*>(s_coef + (qq * K + k) * 4 + 2);
+              const uint32_t mlo = s_m[qq * K + k];
+#pragma unroll
+              for (int v = 0; v < V; ++v)
+                texp_gacc(tb, fma(na[k], c[r][v], nb[k][v]), mlo, g01.x, g01.y, g23.x, g23.y, acc[k][v]);
+            }
           }
         } else {
-          const double* row = reinterpret_cast<const double*>(stages + s * STAGE);
+          for (int r = 0; r < nq; ++r) {
+            const double* row = reinterpret_cast<const double*>(stages + s * STAGE + r * TILE * 8);
+            const int qq = base + r;
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const int lc = l0 + (v >> 1) * PS + (v & 1);
-            if (lc < nloc) {
-              const double cv2 = row[lc];
+            for (int v = 0; v < V; ++v) {
+              const int lc = l0 + (v >> 1) * PS + (v & 1);
+              if (lc < nloc) {
+                const double cv2 = row[lc];
 #pragma unroll
-              for (int k = 0; k < K; ++k) {
-                const double* cf = s_coef + (qq * K + k) * 4;
-                texp_gacc(tb, fma(na[k], cv2, nb[k][v]), s_m[qq * K + k], cf[0], cf[1], cf[2], cf[3], acc[k][v]);
+                for (int k = 0; k < K; ++k) {
+                  const double* cf = s_coef + (qq * K + k) * 4;
+                  texp_gacc(tb, fma(na[k], cv2, nb[k][v]), s_m[qq * K + k], cf[0], cf[1], cf[2], cf[3], acc[k][v]);
+                }
               }
             }
           }
         }
-        mbar_arrive(empty + s);
+        release(empty + s);
       }
     }
 #pragma unroll
@@ -338,14 +358,14 @@ static int launch_rowpass_tma_t(const RowPassArgs& A, cudaStream_t st) {
 
 template <int K>
 static int launch_colpass_tma_t(const ColPassArgs& A, cudaStream_t st) {
-  const int smem = TAB_BYTES + 4 * 8 * TP_THREADS * 8 + 8 * 8 + 128 * K * 4 * 8 + 128 * K * 4;
+  const int smem = TAB_BYTES + 4 * 2 * 4 * TP_THREADS * 8 + 8 * 8 + 128 * K * 4 * 8 + 128 * K * 4;
   auto kern = colpass_tma_kernel<K>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return LEANOT_ECUDA;
     attr = true;
   }
-  const int64_t items = ((A.cost.n + 8 * TP_THREADS - 1) / (8 * TP_THREADS)) * A.splits;
+  const int64_t items = ((A.cost.n + 4 * TP_THREADS - 1) / (4 * TP_THREADS)) * A.splits;
   const int grid = (int)std::min<int64_t>(items, num_sms());
   if (grid < 1) return LEANOT_OK;
   kern<<<grid, TP_ALL, smem, st>>>(A);
