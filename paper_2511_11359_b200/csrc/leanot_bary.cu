@@ -66,6 +66,12 @@ __global__ void bary_dual_reduce_kernel(const double* logz, const double* w, int
   if (threadIdx.x == 0) out[0] = gm + log(s);
 }
 
+// separable grid path (leanot_sep.cu)
+static bool use_sep_bary(const leanot_bary_plan_t& P);
+static int sep_bary_rows(const leanot_bary_plan_t& P, bool eval, cudaStream_t st);
+static int sep_bary_cols(const leanot_bary_plan_t& P, cudaStream_t st);
+static int sep_bary_eval(const leanot_bary_plan_t& P, cudaStream_t st);
+
 static int validate_bary(const leanot_bary_plan_t* P) {
   if (!P) { set_error("null plan"); return LEANOT_EINVAL; }
   LEANOT_TRY(validate_cost(&P->cost));
@@ -150,6 +156,17 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
   cudaStream_t st = S_(stream);
   const int64_t n = P->n, nr = P->row1 - P->row0;
   const int m = P->m;
+  if (use_sep_bary(*P)) {
+    // grid cost: separable O(n^1.5) row normalizers, r-maps, separable column sums
+    LEANOT_TRY(sep_bary_rows(*P, (flags & LEANOT_SWEEP_EVAL) != 0, st));
+    int nblk = (int)std::min<int64_t>((n + 255) / 256, 1024);
+    for (int w = 0; w < 2; ++w) {
+      bary_g_kernel<<<nblk, 256, 0, st>>>(P->L + (int64_t)w * m * nr, m, n, P->w, P->scratch, P->partial);
+      bary_r_kernel<<<1, 1024, 0, st>>>(P->scratch, n, P->partial, nblk, P->r + (int64_t)w * n);
+    }
+    LEANOT_TRY(sep_bary_cols(*P, st));
+    return check_launch("bary_sweep(separable)");
+  }
   for (int k = 0; k < m; ++k) {
     RowPassArgs A = bary_rowpass(*P, k);
     LEANOT_TRY(launch_rowpass(A, 2, (flags & LEANOT_SWEEP_EVAL) != 0, st));
@@ -194,6 +211,10 @@ int leanot_bary_update(const leanot_bary_plan_t* P, void* stream) {
 int leanot_bary_eval(const leanot_bary_plan_t* P, void* stream) {
   LEANOT_TRY(validate_bary(P));
   cudaStream_t st = S_(stream);
+  if (use_sep_bary(*P)) {
+    LEANOT_TRY(sep_bary_eval(*P, st));
+    return check_launch("bary_eval(separable)");
+  }
   const int64_t n = P->n, nr = P->row1 - P->row0;
   const int m = P->m;
   for (int k = 0; k < m; ++k) {

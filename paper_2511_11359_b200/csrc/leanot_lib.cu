@@ -5,3 +5,4 @@
 #include "leanot_bary.cu"
 #include "leanot_sinkhorn.cu"
 #include "leanot_dense.cu"
+#include "leanot_sep.cu"

@@ -435,10 +435,15 @@ static UpdArgs make_upd(const leanot_dxg_plan_t& P) {
   return U;
 }
 
+// separable grid path (leanot_sep.cu)
+static bool use_sep(const leanot_dxg_plan_t& P);
+static int sep_dxg_sweep(const leanot_dxg_plan_t& P, bool eval, cudaStream_t st);
+static int sep_dxg_eval(const leanot_dxg_plan_t& P, cudaStream_t st);
+
 // plans whose O(n) work fits one CTA and whose sweep covers all rows (single process):
-// launch-bound regime, fused update path
+// launch-bound regime, fused update path (reduces the column slabs itself)
 static bool small_plan(const leanot_dxg_plan_t& P) {
-  return P.n <= 16384 && P.row0 == 0 && P.row1 == P.n;
+  return P.n <= 16384 && P.row0 == 0 && P.row1 == P.n && !use_sep(P);
 }
 
 static RowPassArgs make_rowpass(const leanot_dxg_plan_t& P) {
@@ -737,6 +742,12 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
   LEANOT_TRY(validate_plan(P));
   LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
+  if (use_sep(*P)) {
+    // grid cost: O(n^1.5) separable sweep (both phases at once; phase flags ignored)
+    if (flags & LEANOT_SWEEP_ROWS_ONLY) return LEANOT_OK;
+    LEANOT_TRY(sep_dxg_sweep(*P, (flags & LEANOT_SWEEP_EVAL) != 0, st));
+    return check_launch("dxg_sweep(separable)");
+  }
   RowPassArgs A = make_rowpass(*P);
   if (!(flags & LEANOT_SWEEP_COLS_ONLY)) LEANOT_TRY(launch_rowpass(A, 2, (flags & LEANOT_SWEEP_EVAL) != 0, st));
   if (flags & LEANOT_SWEEP_ROWS_ONLY) return check_launch("dxg_sweep(rows)");
@@ -770,6 +781,10 @@ int leanot_dxg_update(const leanot_dxg_plan_t* P, void* stream) {
 int leanot_dxg_eval(const leanot_dxg_plan_t* P, void* stream) {
   LEANOT_TRY(validate_plan(P));
   cudaStream_t st = S_(stream);
+  if (use_sep(*P)) {
+    LEANOT_TRY(sep_dxg_eval(*P, st));
+    return check_launch("dxg_eval(separable)");
+  }
   const int64_t nr = P->row1 - P->row0;
   const double* v = P->rowstat + 2 * nr;  // row minima (eta = 0 form)
   if (P->prm.eta > 0) {

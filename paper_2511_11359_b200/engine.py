@@ -98,7 +98,10 @@ class DxgEngine:
         self.S = torch.zeros(2 * nr, **f64)
         self.coef = torch.zeros(8 * nr, **f64)
         self.rowstat = torch.zeros(3 * nr, **f64)
-        self.slab = torch.zeros(splits * 2 * n, **f64)
+        slab = splits * 2 * n
+        if kernel.cost_struct().kind == _lib.COST_GRID:   # separable path scratch (leanot_sep.cu)
+            slab = max(slab, int(L.leanot_grid_sep_ws_doubles(kernel.cost_struct())))
+        self.slab = torch.zeros(slab, **f64)
         self.col = torch.zeros(2 * n, **f64)
         self.partial = torch.zeros(2 * nblk, **f64)
         self.evalbuf = torch.zeros(16, **f64)
