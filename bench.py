@@ -314,7 +314,7 @@ def run_b200(args):
 
     # end to end through the public step API with host state (dxg.dxg_step)
     if not args.no_e2e and world == 1:
-        kc = core.HashKernel(n, seed=args.seed) if False else kern
+        kc = kern
         st = dxg.DxgState(dxg.LogOddsField(np.zeros(n)), dxg.TransportLogWeights(0.0, np.zeros(n), 0.0, 0))
         rh, ch = core.Histogram(r), core.Histogram(c)
         for _ in range(2):

@@ -17,7 +17,6 @@ deterministic), plus 3 scalars on evaluation iterations.
 from __future__ import annotations
 
 import ctypes as C
-import math
 
 import numpy as np
 
@@ -241,7 +240,3 @@ def default_group():
         pass
     return None
 
-
-def check_finite(x, what):
-    if not math.isfinite(x):
-        raise RuntimeError(f"non-finite {what}")
