@@ -196,6 +196,7 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
 
 int leanot_bary_update(const leanot_bary_plan_t* P, void* stream) {
   LEANOT_TRY(validate_bary(P));
+  LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
   for (int k = 0; k < P->m; ++k) {
     UpdArgs U = bary_upd(*P, k);
@@ -210,6 +211,7 @@ int leanot_bary_update(const leanot_bary_plan_t* P, void* stream) {
 // [127] LSE_i of the dual's g (barycenter.py:193-195)
 int leanot_bary_eval(const leanot_bary_plan_t* P, void* stream) {
   LEANOT_TRY(validate_bary(P));
+  LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
   if (use_sep_bary(*P)) {
     LEANOT_TRY(sep_bary_eval(*P, st));

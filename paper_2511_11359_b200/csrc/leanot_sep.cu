@@ -14,10 +14,18 @@
 namespace leanot {
 
 // Y[p][q] = LSE_{q'} (X[p][q'] + g[|q-q'|])  (axis 1)   or   LSE_{p'} (X[p'][q] + g[|p-p'|])  (axis 0)
-// MIN mode: min instead of LSE.  One thread per output; two passes (max, then shifted sum).
+// MIN mode: min instead of LSE.  One thread per output; two passes (exact max, then the
+// max-shifted sum with the table exp of leanot_common.cuh, zero integer shift).
 template <bool MIN>
-__global__ void sep_axis_kernel(const double* __restrict__ X, const double* __restrict__ g, int H, int W, int axis,
-                                double* __restrict__ Y) {
+__global__ void __launch_bounds__(256) sep_axis_kernel(const double* __restrict__ X, const double* __restrict__ g,
+                                                       int H, int W, int axis, double* __restrict__ Y) {
+  extern __shared__ __align__(16) char smem[];
+  uint32_t tb = 0;
+  if (!MIN) {
+    load_table(reinterpret_cast<double*>(smem));
+    __syncthreads();
+    tb = lane_tab_addr(smem);
+  }
   const int64_t total = (int64_t)H * W;
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
     const int p = (int)(o / W), q = (int)(o % W);
@@ -35,7 +43,8 @@ __global__ void sep_axis_kernel(const double* __restrict__ X, const double* __re
       continue;
     }
     double s = 0.0;
-    for (int t = 0; t < len; ++t) s += exp(base[t * stride] + g[abs(pos - t)] - m);
+#pragma unroll 4
+    for (int t = 0; t < len; ++t) texp_acc(tb, fmax(base[t * stride] + g[abs(pos - t)] - m, -1000.0), 0u, s);
     Y[o] = m + log(s);
   }
 }
@@ -105,8 +114,16 @@ struct SepCtx {
   cudaStream_t st;
   int nb;
   void axis(const double* X, const double* g, int ax, double* Y, bool mn = false) const {
-    if (mn) sep_axis_kernel<true><<<nb, 256, 0, st>>>(X, g, H, W, ax, Y);
-    else sep_axis_kernel<false><<<nb, 256, 0, st>>>(X, g, H, W, ax, Y);
+    if (mn) {
+      sep_axis_kernel<true><<<nb, 256, 0, st>>>(X, g, H, W, ax, Y);
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(sep_axis_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES);
+        attr = true;
+      }
+      sep_axis_kernel<false><<<nb, 256, TAB_BYTES, st>>>(X, g, H, W, ax, Y);
+    }
   }
   void table(const double* a_ptr, int mode, double* g, double eta = 1.0) const {
     const int D = H > W ? H : W;
@@ -118,7 +135,7 @@ struct SepCtx {
 static SepCtx make_sep(const leanot_cost_t& c, cudaStream_t st) {
   SepCtx s;
   s.H = c.height; s.W = c.width; s.p = c.p; s.n = c.n; s.inv = c.inv_scale; s.st = st;
-  s.nb = (int)std::min<int64_t>((c.n + 255) / 256, 4096);
+  s.nb = (int)std::min<int64_t>((c.n + 255) / 256, (int64_t)num_sms() * 3);
   return s;
 }
 
@@ -306,6 +323,7 @@ int leanot_grid_sep_lse(const leanot_cost_t* cost, const double* a_dev, const do
   using namespace leanot;
   LEANOT_TRY(validate_cost(cost));
   if (cost->kind != LEANOT_COST_GRID) { set_error("separable path needs a grid cost"); return LEANOT_EINVAL; }
+  LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
   const SepCtx s = make_sep(*cost, st);
   const int64_t n = cost->n;
@@ -322,6 +340,7 @@ int leanot_grid_sep_colsum(const leanot_cost_t* cost, const double* a_dev, const
   using namespace leanot;
   LEANOT_TRY(validate_cost(cost));
   if (cost->kind != LEANOT_COST_GRID) { set_error("separable path needs a grid cost"); return LEANOT_EINVAL; }
+  LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
   const SepCtx s = make_sep(*cost, st);
   const int64_t n = cost->n;

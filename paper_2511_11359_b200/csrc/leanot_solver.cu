@@ -765,6 +765,7 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
 
 int leanot_dxg_update(const leanot_dxg_plan_t* P, void* stream) {
   LEANOT_TRY(validate_plan(P));
+  LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
   UpdArgs U = make_upd(*P);
   if (small_plan(*P)) {
@@ -780,6 +781,7 @@ int leanot_dxg_update(const leanot_dxg_plan_t* P, void* stream) {
 
 int leanot_dxg_eval(const leanot_dxg_plan_t* P, void* stream) {
   LEANOT_TRY(validate_plan(P));
+  LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
   if (use_sep(*P)) {
     LEANOT_TRY(sep_dxg_eval(*P, st));
