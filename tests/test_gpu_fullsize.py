@@ -10,8 +10,8 @@ that hold for any n:
   * mass conservation: sum_j col_j == sum_i r_i for both half-step weight sets;
   * O(n) update: the GPU's next state equals the oracle's dual_md_step /
     _advance_weights (dxg.py:223-258) applied to the GPU's own columns;
-  * determinism: two sweeps of the same state are bitwise identical;
-  * shard additivity: the two row shards' partials summed in rank order equal
+  * determinism: two sweeps of the same state (same row shifts) are bitwise identical;
+  * shard additivity: row-shard partials summed in rank order equal
     the unsharded columns (engine.combine_partials, multi-GPU path).
 """
 
@@ -91,6 +91,7 @@ def test_config3_full_size_properties(a):
         k = core.HashKernel(n, seed=7)
         eng = _engine(k, r, c, prm, st)
         col_now, col_bar = _cols(eng)
+        eng.load_state(*st)             # same state, same (exact row-max) shifts
         again = _cols(eng)
         assert np.array_equal(col_now, again[0]) and np.array_equal(col_bar, again[1])   # deterministic
         for col in (col_now, col_bar):
