@@ -35,6 +35,11 @@ constexpr double EC1 = 1.0000000000000024;
 constexpr double EC2 = 0.5000000190914873;
 constexpr double EC3 = 0.16666666285067583;
 
+// The same coefficients in the constant bank: a DFMA takes one constant-bank operand
+// directly, so the hot loops do not re-materialize 64-bit immediates per stage.
+__constant__ double c_lstep = LSTEP;
+__constant__ double c_ec0 = EC0, c_ec1 = EC1, c_ec3 = EC3;
+
 // Biased table: entry j holds 2^(j/512) (correctly rounded) with (j << 11) subtracted
 // from its high word.  For kk = 512 e + j the scaled value 2^(kk/512) then has
 // high word  hi(T'[j]) + (kk << 11)  -- one LEA, no masking -- because
@@ -72,20 +77,20 @@ __device__ __forceinline__ double tab_scaled(uint32_t tb, double t, uint32_t mlo
 __device__ __forceinline__ double texp(uint32_t tb, double x, uint32_t mlo) {
   const double t = fma(x, KINV, MAGIC);
   const double kd = t - MAGIC;
-  const double r = fma(kd, -LSTEP, x);
+  const double r = fma(kd, -c_lstep, x);
   const double T = tab_scaled(tb, t, mlo);
-  const double p = fma(fma(EC3, r, EC2), r, EC1);
-  return T * fma(r, p, EC0);
+  const double p = fma(fma(c_ec3, r, EC2), r, c_ec1);
+  return T * fma(r, p, c_ec0);
 }
 
 // acc += exp(x - m*LSTEP)
 __device__ __forceinline__ void texp_acc(uint32_t tb, double x, uint32_t mlo, double& acc) {
   const double t = fma(x, KINV, MAGIC);
   const double kd = t - MAGIC;
-  const double r = fma(kd, -LSTEP, x);
+  const double r = fma(kd, -c_lstep, x);
   const double T = tab_scaled(tb, t, mlo);
-  const double p = fma(fma(EC3, r, EC2), r, EC1);
-  acc = fma(T, fma(r, p, EC0), acc);
+  const double p = fma(fma(c_ec3, r, EC2), r, c_ec1);
+  acc = fma(T, fma(r, p, c_ec0), acc);
 }
 
 // acc += g * exp(x - m*LSTEP) with g folded into the polynomial: gc = g*{EC0..EC3}
@@ -93,7 +98,7 @@ __device__ __forceinline__ void texp_gacc(uint32_t tb, double x, uint32_t mlo, d
                                           double g3, double& acc) {
   const double t = fma(x, KINV, MAGIC);
   const double kd = t - MAGIC;
-  const double r = fma(kd, -LSTEP, x);
+  const double r = fma(kd, -c_lstep, x);
   const double T = tab_scaled(tb, t, mlo);
   const double q = fma(fma(fma(g3, r, g2), r, g1), r, g0);
   acc = fma(T, q, acc);

@@ -42,6 +42,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void release_u32(uint32_t bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 // a warp releases a stage once all its lanes are done reading it (one arrival per warp)
 __device__ __forceinline__ void release(uint64_t* bar) {
   __syncwarp();
@@ -102,7 +114,12 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
   double na[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) na[k] = -A.a[k];
-  uint32_t q = 0;
+  // ring position, kept incrementally (no division by NS, 32-bit counters) so the
+  // per-stage bookkeeping stays small next to the 16 exps a thread does per stage
+  uint32_t s = 0, ph = 0;
+  const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+  const char* const st_base = stages + 16 * threadIdx.x;
+  const int n32 = (int)n, nch32 = (int)nch;
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int64_t ib = A.i0 + blk * R;
     uint32_t mlo[R][K];
@@ -119,12 +136,12 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[r][k] = 0.0;
     }
-    for (int64_t ch = 0; ch < nch; ++ch, ++q) {
-      const int s = q % NS;
-      mbar_wait(full + s, (q / NS) & 1);
-      const int64_t j = ch * CH + 2 * threadIdx.x;
-      if (j < n) {
-        const char* st = stages + s * STAGE + 16 * threadIdx.x;
+    int j = 2 * threadIdx.x;
+#pragma unroll 2
+    for (int ch = 0; ch < nch32; ++ch, j += CH) {
+      mbar_wait_u32(full_u + 8 * s, ph);
+      if (j < n32) {
+        const char* st = st_base + s * STAGE;
         double2 bv[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) bv[k] = *reinterpret_cast<const double2*>(st + (R + k) * CH * 8);
@@ -152,7 +169,8 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
           }
         }
       }
-      release(empty + s);
+      release_u32(empty_u + 8 * s);
+      if (++s == NS) { s = 0; ph ^= 1; }
     }
     // block reduction over the consumer warps, fixed order
 #pragma unroll

@@ -50,6 +50,9 @@ for _ in range(a.iters):
     torch.cuda.synchronize()
     ta.append(e[0].elapsed_time(e[1])); tb.append(e[1].elapsed_time(e[2]))
 smi.terminate()
-clk = [float(line.split(",")[0]) for line in smi.stdout.read().splitlines() if line.strip()]
+rows = [line.split(",") for line in smi.stdout.read().splitlines() if line.strip()]
+clk = [float(x[0]) for x in rows]
+pw = [float(x[1]) for x in rows]
 print(json.dumps({"tag": a.tag, "n": n, "kind": a.kind, "rowpass_ms": statistics.median(ta),
-                  "colpass_ms": statistics.median(tb), "sm_mhz": statistics.median(clk) if clk else None}))
+                  "colpass_ms": statistics.median(tb), "sm_mhz": statistics.median(clk) if clk else None,
+                  "power_w": statistics.median(pw) if pw else None}))
