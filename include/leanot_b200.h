@@ -238,12 +238,15 @@ int leanot_plan_cost(const leanot_cost_t* cost, const double* P, int64_t ld, dou
  * C_ij = (f(|dr|) + f(|dc|))/scale factorizes, so each n^2 LSE is two 1-D LSE convolutions.
  * The DXG sweep/eval entry points use it automatically for single-process grid plans
  * (LEANOT_GRID_SEPARABLE=0 forces the dense sweeps); the slab of such plans must hold
- * leanot_grid_sep_ws_doubles() doubles. */
+ * leanot_grid_sep_ws_doubles() doubles.  Each LSE convolution runs as an FP64 tensor-core
+ * (DMMA) GEMM in the linear domain when its kernel table stays within e^+-600, else as an
+ * exact log-domain reduction; the choice is made on device (LEANOT_SEP_GEMM=0 forces the
+ * log domain). */
 int64_t leanot_grid_sep_ws_doubles(const leanot_cost_t* cost);
-/* L_i = LSE_j(-(a C_ij + b_j)), a in device memory; ws >= 2n + max(H,W) doubles */
+/* L_i = LSE_j(-(a C_ij + b_j)), a in device memory; ws >= leanot_grid_sep_ws_doubles(cost) doubles */
 int leanot_grid_sep_lse(const leanot_cost_t* cost, const double* a_dev, const double* b, double* L, double* ws,
                         void* stream);
-/* col_j = exp(-b_j) sum_i exp(logw_i - a C_ij); ws >= 2n + max(H,W) doubles */
+/* col_j = exp(-b_j) sum_i exp(logw_i - a C_ij); ws >= leanot_grid_sep_ws_doubles(cost) doubles */
 int leanot_grid_sep_colsum(const leanot_cost_t* cost, const double* a_dev, const double* b, const double* logw,
                            double* col, double* ws, void* stream);
 

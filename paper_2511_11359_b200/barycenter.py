@@ -118,7 +118,7 @@ class BaryEngine:
         self.rowstat = z(3 * m * n)
         slab = splits * 2 * n
         if kernel.cost_struct().kind == _lib.COST_GRID:   # separable path scratch (leanot_sep.cu)
-            slab = max(slab, int(L.leanot_grid_sep_ws_doubles(kernel.cost_struct())) + 4 * n)
+            slab = max(slab, int(L.leanot_grid_sep_ws_doubles(kernel.cost_struct())) + 4 * m * n)
         self.slab = z(slab)
         self.col = z(2 * m * n)
         self.partial = z(2 * max(nblk, (n + 255) // 256) + 2048)
