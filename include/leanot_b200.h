@@ -201,7 +201,8 @@ int leanot_bary_prepare(const leanot_bary_plan_t* plan, double a, double s, doub
 int leanot_bary_sweep(const leanot_bary_plan_t* plan, int flags, void* stream);
 int leanot_bary_update(const leanot_bary_plan_t* plan, void* stream);
 int leanot_bary_eval(const leanot_bary_plan_t* plan, void* stream);
-/* r_i proportional to exp(sum_k w_k L_ki), k-sum in sorted order (barycenter.py:90-97) */
+/* r_i proportional to exp(sum_k w_k L_ki), k-sum in sorted order (barycenter.py:90-97);
+ * scratch >= n + 2048 doubles */
 int leanot_bary_rmap(const double* L, int m, int64_t n, const double* w, double* r, double* scratch, void* stream);
 
 /* ---- Sinkhorn / IBP baselines (sinkhorn.py:47-228) -- */

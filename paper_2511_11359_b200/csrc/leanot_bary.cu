@@ -159,11 +159,8 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
   if (use_sep_bary(*P)) {
     // grid cost: separable O(n^1.5) row normalizers, r-maps, separable column sums
     LEANOT_TRY(sep_bary_rows(*P, (flags & LEANOT_SWEEP_EVAL) != 0, st));
-    int nblk = (int)std::min<int64_t>((n + 255) / 256, 1024);
-    for (int w = 0; w < 2; ++w) {
-      bary_g_kernel<<<nblk, 256, 0, st>>>(P->L + (int64_t)w * m * nr, m, n, P->w, P->scratch, P->partial);
-      bary_r_kernel<<<1, 1024, 0, st>>>(P->scratch, n, P->partial, nblk, P->r + (int64_t)w * n);
-    }
+    for (int w = 0; w < 2; ++w)
+      launch_rmap(P->L + (int64_t)w * m * nr, m, n, P->w, P->scratch, P->partial, P->r + (int64_t)w * n, st);
     LEANOT_TRY(sep_bary_cols(*P, st));
     return check_launch("bary_sweep(separable)");
   }
@@ -175,11 +172,8 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
   const int g = (int)std::min<int64_t>((tot + 255) / 256, 4096);
   bary_lse_kernel<<<g, 256, 0, st>>>(P->mu, P->S, m, nr, P->L);
   // r_now from the current weights, r_bar from the midpoint weights (barycenter.py:126, 137)
-  int nblk = (int)std::min<int64_t>((n + 255) / 256, 1024);
-  for (int w = 0; w < 2; ++w) {
-    bary_g_kernel<<<nblk, 256, 0, st>>>(P->L + (int64_t)w * m * nr, m, n, P->w, P->scratch, P->partial);
-    bary_r_kernel<<<1, 1024, 0, st>>>(P->scratch, n, P->partial, nblk, P->r + (int64_t)w * n);
-  }
+  for (int w = 0; w < 2; ++w)
+    launch_rmap(P->L + (int64_t)w * m * nr, m, n, P->w, P->scratch, P->partial, P->r + (int64_t)w * n, st);
   bary_coef_kernel<<<g, 256, 0, st>>>(P->S, P->r, m, nr, P->row0, n, P->coef);
   for (int k = 0; k < m; ++k) {
     ColPassArgs B;

@@ -332,16 +332,40 @@ __global__ void bary_g_kernel(const double* L, int m, int64_t n, const double* w
   block_max_store(mx, partial + blockIdx.x);
 }
 
-__global__ void bary_r_kernel(const double* g, int64_t n, const double* partial, int nblk, double* r) {
+// e_i = exp(g_i - max g) and per-block partial sums (partial[0..nblk) holds the block maxima)
+__global__ void bary_e_kernel(const double* g, int64_t n, const double* partial, int nblk, double* r, double* psum) {
   const double M = max_of(partial, nblk);
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double e = exp(g[i] - M);
     r[i] = e;
     s += e;
   }
   s = block_sum(s);
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) r[i] = r[i] / s;
+  if (threadIdx.x == 0) psum[blockIdx.x] = s;
+}
+
+// r_i /= sum of the block partial sums, added in block order by every block (deterministic)
+__global__ void bary_norm_kernel(double* r, int64_t n, const double* psum, int nblk) {
+  __shared__ double tot;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < nblk; ++b) t += psum[b];
+    tot = t;
+  }
+  __syncthreads();
+  const double s = tot;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = r[i] / s;
+}
+
+// full r-map over all SMs; partial needs 2 * nblk doubles (nblk <= 1024)
+static void launch_rmap(const double* L, int m, int64_t n, const double* w, double* g, double* partial, double* r,
+                        cudaStream_t st) {
+  const int nblk = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  bary_g_kernel<<<nblk, 256, 0, st>>>(L, m, n, w, g, partial);
+  bary_e_kernel<<<nblk, 256, 0, st>>>(g, n, partial, nblk, r, partial + nblk);
+  bary_norm_kernel<<<nblk, 256, 0, st>>>(r, n, partial + nblk, nblk);
 }
 
 // ---------------------------------------------------------------------------
@@ -850,11 +874,7 @@ int leanot_bary_rmap(const double* L, int m, int64_t n, const double* w, double*
   LEANOT_TRY(ensure_init());
   if (m < 1 || m > LEANOT_MAX_K) { set_error("barycenter supports 1..16 marginals"); return LEANOT_EINVAL; }
   cudaStream_t st = S_(stream);
-  int nblk = (int)std::min<int64_t>((n + 255) / 256, 1024);
-  double* g = scratch;
-  double* partial = scratch + n;
-  bary_g_kernel<<<nblk, 256, 0, st>>>(L, m, n, w, g, partial);
-  bary_r_kernel<<<1, 1024, 0, st>>>(g, n, partial, nblk, r);
+  launch_rmap(L, m, n, w, scratch, scratch + n, r, st);
   return check_launch("bary_rmap");
 }
 
