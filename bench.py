@@ -81,9 +81,10 @@ class ClockSampler:
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw.instant,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                 "clocks_event_reasons.sw_power_cap,enforced.power.limit", "--format=csv,noheader,nounits",
+                 "-lms", "100"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -97,7 +98,7 @@ class ClockSampler:
     def summary(self):
         self.f.flush()
         self.f.seek(0)
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw, lim = [], 0.0, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.f.read().splitlines():
             parts = [x.strip() for x in line.split(",")]
@@ -108,12 +109,21 @@ class ClockSampler:
                 mx = max(mx, float(parts[1]))
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+                lim = float(parts[7])
+            except (ValueError, IndexError):
+                pass
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if pw:
+            out["power_w"] = statistics.median(pw)     # board power during the timed region
+            out["power_limit_w"] = lim
+        return out
 
 
 # ---------------------------------------------------------------------------

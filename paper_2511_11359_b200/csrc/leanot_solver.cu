@@ -159,10 +159,9 @@ __global__ void dxg_update2(const UpdArgs U, int advance_scalars) {
   }
 }
 
-// Small n (launch-bound): slab reduce + K3 + K4 + K5 in one CTA (same arithmetic, same order
-// of operations per element; maxima are order-independent).
-__global__ void __launch_bounds__(1024) dxg_update_small(const UpdArgs U, const double* slab, int splits,
-                                                         double* col) {
+// Small n (launch-bound): K3 + K4 + K5 in one CTA on the reduced columns (same arithmetic,
+// same order of operations per element; maxima are order-independent).
+__global__ void __launch_bounds__(1024) dxg_update_small(const UpdArgs U) {
   __shared__ double red[32];
   __shared__ double bc;
   const int64_t n = U.n;
@@ -182,10 +181,7 @@ __global__ void __launch_bounds__(1024) dxg_update_small(const UpdArgs U, const 
   };
   double mx = -INFINITY;
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    double cn = 0.0, cb = 0.0;
-    for (int q = 0; q < splits; ++q) { cn += slab[(q * 2) * n + j]; cb += slab[(q * 2 + 1) * n + j]; }
-    col[j] = cn;
-    col[n + j] = cb;
+    const double cn = U.col[j], cb = U.col[n + j];
     const double cj = U.c[j], ctj = U.ct[j], dj = U.delta[j];
     const double dbar = md_step(U.A, U.B, dj, cn, cj, ctj);
     double dn = md_step(U.A, U.B, dj, cb, cj, ctj);
@@ -781,9 +777,7 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
   B.b[0] = P->b; B.b[1] = P->b_bar;
   B.m = P->m; B.coef = P->coef; B.slab = P->slab; B.splits = P->splits;
   LEANOT_TRY(launch_colpass(B, 2, st));
-  // small single-process plans fold the slab reduce into dxg_update_small, except on
-  // evaluation sweeps whose column marginal is read before the update
-  if (!small_plan(*P) || (flags & LEANOT_SWEEP_EVAL)) LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, P->n, P->col, st));
+  LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, P->n, P->col, st));
   return check_launch("dxg_sweep");
 }
 
@@ -793,8 +787,8 @@ int leanot_dxg_update(const leanot_dxg_plan_t* P, void* stream) {
   cudaStream_t st = S_(stream);
   UpdArgs U = make_upd(*P);
   if (small_plan(*P)) {
-    // slabs -> col (again, if an eval sweep already reduced them: same values) + all O(n) updates
-    dxg_update_small<<<1, 1024, 0, st>>>(U, P->slab, P->splits, P->col);
+    // all O(n) updates in one CTA (the sweep already reduced the slabs into col)
+    dxg_update_small<<<1, 1024, 0, st>>>(U);
     return check_launch("dxg_update_small");
   }
   dxg_update1<<<P->nblk_upd, 256, 0, st>>>(U);

@@ -414,13 +414,27 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
   }
 }
 
-// col[k][j] = sum over splits in fixed order
-__global__ void slab_reduce_kernel(const double* __restrict__ slab, int splits, int K, int64_t n, double* __restrict__ col) {
+// col[k][j] = sum over splits in a fixed order: 32 outputs x 8 split groups per block; group g
+// adds splits g, g+8, ... in increasing order, then the 8 group sums are added in group order.
+__global__ void __launch_bounds__(256) slab_reduce_kernel(const double* __restrict__ slab, int splits, int K,
+                                                          int64_t n, double* __restrict__ col) {
+  __shared__ double part[8][33];
   const int64_t total = (int64_t)K * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+  const int o = threadIdx.x & 31, g = threadIdx.x >> 5;
+  for (int64_t t0 = (int64_t)blockIdx.x * 32; t0 < total; t0 += (int64_t)gridDim.x * 32) {
+    const int64_t t = t0 + o;
     double s = 0.0;
-    for (int q = 0; q < splits; ++q) s += slab[q * total + t];
-    col[t] = s;
+    if (t < total)
+      for (int q = g; q < splits; q += 8) s += slab[q * total + t];
+    part[g][o] = s;
+    __syncthreads();
+    if (g == 0 && t < total) {
+      double v = part[0][o];
+#pragma unroll
+      for (int h = 1; h < 8; ++h) v += part[h][o];
+      col[t] = v;
+    }
+    __syncthreads();
   }
 }
 
@@ -683,7 +697,7 @@ int launch_colpass(const ColPassArgs& A, int K, cudaStream_t st) {
 
 int launch_slab_reduce(const double* slab, int splits, int K, int64_t n, double* col, cudaStream_t st) {
   const int64_t total = (int64_t)K * n;
-  int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 4);
+  int grid = (int)std::min<int64_t>((total + 31) / 32, (int64_t)num_sms() * 8);
   if (grid < 1) return LEANOT_OK;
   slab_reduce_kernel<<<grid, 256, 0, st>>>(slab, splits, K, n, col);
   return LEANOT_OK;
