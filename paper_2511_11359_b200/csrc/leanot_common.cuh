@@ -48,8 +48,13 @@ __constant__ double c_ec0 = EC0, c_ec1 = EC1, c_ec3 = EC3;
 // this definition exists exactly once.
 __device__ double g_exp2_table[NTAB];
 
+// One global read per entry, replicated with 16-byte stores (entry j occupies the 128 B
+// at smem_tab + 16 j: one copy per lane of a half-warp).
 __device__ __forceinline__ void load_table(double* smem_tab) {
-  for (int i = threadIdx.x; i < NTAB * TAB_LANES; i += blockDim.x) smem_tab[i] = g_exp2_table[i >> 4];
+  for (int i = threadIdx.x; i < NTAB * (TAB_LANES / 2); i += blockDim.x) {
+    const double v = g_exp2_table[i / (TAB_LANES / 2)];
+    reinterpret_cast<double2*>(smem_tab)[i] = make_double2(v, v);
+  }
 }
 
 // Shared-window address of this lane's replica of the table (base + lane*8), opaque

@@ -6,3 +6,4 @@
 #include "leanot_sinkhorn.cu"
 #include "leanot_dense.cu"
 #include "leanot_sep.cu"
+#include "leanot_persist.cu"

@@ -459,6 +459,8 @@ static UpdArgs make_upd(const leanot_dxg_plan_t& P) {
 static bool use_sep(const leanot_dxg_plan_t& P);
 static int sep_dxg_sweep(const leanot_dxg_plan_t& P, bool eval, cudaStream_t st);
 static int sep_dxg_eval(const leanot_dxg_plan_t& P, cudaStream_t st);
+// persistent small-n iterations (leanot_persist.cu)
+static int try_persist_iterate(const leanot_dxg_plan_t& P, int iters, cudaStream_t st);
 
 // plans whose O(n) work fits one CTA and whose sweep covers all rows (single process):
 // launch-bound regime, fused update path (reduces the column slabs itself)
@@ -819,6 +821,9 @@ int leanot_dxg_eval(const leanot_dxg_plan_t* P, void* stream) {
 }
 
 int leanot_dxg_iterate(const leanot_dxg_plan_t* P, int iters, void* stream) {
+  LEANOT_TRY(validate_plan(P));
+  LEANOT_TRY(ensure_init());
+  if (try_persist_iterate(*P, iters, S_(stream)) == LEANOT_OK) return check_launch("dxg_iterate(persistent)");
   for (int i = 0; i < iters; ++i) {
     LEANOT_TRY(leanot_dxg_sweep(P, 0, stream));
     LEANOT_TRY(leanot_dxg_update(P, stream));

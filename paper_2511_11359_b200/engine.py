@@ -16,6 +16,8 @@ deterministic), plus 3 scalars on evaluation iterations.
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 
 import numpy as np
@@ -180,7 +182,9 @@ class DxgEngine:
             return
         L = _lib.lib()
         if use_graph is None:
-            use_graph = self.n <= 20000
+            # n <= 4096: leanot_dxg_iterate runs all iterations in one persistent kernel
+            persistent = self.n <= 4096 and os.environ.get("LEANOT_PERSIST", "1") != "0"
+            use_graph = self.n <= 20000 and not persistent
         with _torch().cuda.device(self.device):
             if not use_graph:
                 _lib.check(L.leanot_dxg_iterate(C.byref(self.plan), int(iters), self._stream()), "dxg_iterate")

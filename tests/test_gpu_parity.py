@@ -217,3 +217,28 @@ def test_config1_same_iteration_count_as_reference():
     assert rel_err(got[:, 2], ref[:, 2]) <= 1e-8
     assert abs(sol.final.primal - ref[-1, 1]) <= 1e-8 * abs(ref[-1, 1])   # final transport cost
     assert rel_err(sol.state.mu.delta, d["delta"]) <= 1e-8
+
+
+@pytest.mark.parametrize("kind,n", [("explicit", 1000), ("points", 513), ("explicit", 37)])
+def test_persistent_iterations_match_launch_per_kernel_path(kind, n):
+    """n <= 4096: leanot_dxg_iterate runs all iterations in one cooperative kernel; it must
+    track the regular kernels (graph of sweep + update launches) iteration by iteration."""
+    dxg = _dxg()
+    from paper_2511_11359_b200 import core
+    from paper_2511_11359_b200.engine import DxgEngine
+    rng = np.random.default_rng(n)
+    k = core.ExplicitKernel(rng.random((n, n))) if kind == "explicit" else core.ColorKernel(rng.random((n, 3)), 2)
+    r, c = O.normalized_hist(rng.random(n)), O.normalized_hist(rng.random(n))
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    delta = rng.uniform(-1, 1, n)
+    b = -np.abs(rng.normal(0, 30, n))
+    b -= b.max()
+    out = []
+    for graph in (False, True):
+        eng = DxgEngine(k, r, c, prm)
+        eng.load_state(delta, b, 60.0, 0.1, 60)
+        eng.iterate(50, use_graph=graph)
+        out.append(eng.read_state())
+    (d0, b0, a0, s0, t0), (d1, b1, a1, s1, t1) = out
+    assert rel_err(d0, d1) <= 1e-11 and rel_err(b0, b1) <= 1e-11
+    assert a0 == a1 and s0 == s1 and t0 == t1 == 110

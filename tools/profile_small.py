@@ -34,3 +34,12 @@ eng.iterate(200, use_graph=True)
 e1.record(st)
 torch.cuda.synchronize()
 print("us per iteration (graph of 200):", e0.elapsed_time(e1) * 1e3 / 200)
+for chunk in (24, 200):
+    eng.iterate(chunk, use_graph=False)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(200 // chunk):
+        eng.iterate(chunk, use_graph=False)
+    e1.record(st)
+    torch.cuda.synchronize()
+    print(f"us per iteration (leanot_dxg_iterate, chunks of {chunk}):", e0.elapsed_time(e1) * 1e3 / (chunk * (200 // chunk)))
