@@ -118,10 +118,11 @@ class BaryEngine:
         self.rowstat = z(3 * m * n)
         slab = splits * 2 * n
         if kernel.cost_struct().kind == _lib.COST_GRID:   # separable path scratch (leanot_sep.cu)
-            slab = max(slab, int(L.leanot_grid_sep_ws_doubles(kernel.cost_struct())) + 4 * m * n)
+            cs = kernel.cost_struct()
+            slab = max(slab, int(L.leanot_grid_sep_ws_doubles(cs)) + 5 * m * n + m * max(cs.height, cs.width))
         self.slab = z(slab)
         self.col = z(2 * m * n)
-        self.partial = z(2 * max(nblk, (n + 255) // 256) + 2048)
+        self.partial = z(2 * m * max(nblk, (n + 255) // 256) + 2048)   # batched update: 2 nblk per marginal
         self.scratch = z(n)
         self.evalbuf = z(128)
         self.flags = torch.zeros(2 + 4 * n, dtype=torch.int32, device=dev)

@@ -103,6 +103,8 @@ static UpdArgs bary_upd(const leanot_bary_plan_t& P, int k) {
   U.tau_p = q.tau_p;
   U.tau_p_eta = q.tau_p * q.eta;
   U.nblk = P.nblk_upd;
+  U.zs_col = 2 * n;
+  U.zs_vec = ns;
   return U;
 }
 
@@ -192,12 +194,12 @@ int leanot_bary_update(const leanot_bary_plan_t* P, void* stream) {
   LEANOT_TRY(validate_bary(P));
   LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
-  for (int k = 0; k < P->m; ++k) {
-    UpdArgs U = bary_upd(*P, k);
-    dxg_update1<<<P->nblk_upd, 256, 0, st>>>(U);
-    dxg_update2<<<P->nblk_upd, 256, 0, st>>>(U, k == P->m - 1 ? 1 : 0);
-    dxg_update3<<<P->nblk_upd, 256, 0, st>>>(U);
-  }
+  // all m marginals in one launch per step (blockIdx.y = k); the shared scalars advance once
+  const UpdArgs U = bary_upd(*P, 0);
+  const dim3 g(P->nblk_upd, P->m);
+  dxg_update1<<<g, 256, 0, st>>>(U);
+  dxg_update2<<<g, 256, 0, st>>>(U, 1);
+  dxg_update3<<<g, 256, 0, st>>>(U);
   return check_launch("bary_update");
 }
 

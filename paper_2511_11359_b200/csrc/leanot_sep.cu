@@ -100,130 +100,144 @@ __global__ void sep_kmat_kernel(const double* __restrict__ g, int L, int D, int 
   }
 }
 
+// Linear-domain operand of one LSE-convolution stage (batched over blockIdx.z, grid cells
+// row-major H x W):  M = exact max over the summed axis, E = exp(X - M) (0 where M = -inf).
+//   AX = 1: one warp per grid row p, M[p] = max_t X[p][t]
+//   AX = 0: 32 grid columns x 32 row groups per block, M[q] = max_p X[p][q]
+template <int AX>
+__global__ void __launch_bounds__(1024) sep_maxexp_kernel(const double* __restrict__ X, int H, int W, int64_t xs,
+                                                         double* __restrict__ E, double* __restrict__ M, int md,
+                                                         const int* __restrict__ lin) {
+  if (!*lin) return;
+  const int64_t n = (int64_t)H * W;
+  X += blockIdx.z * xs;
+  E += blockIdx.z * n;
+  M += (int64_t)blockIdx.z * md;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (AX == 1) {
+    const int p = blockIdx.x * 8 + warp;
+    if (p >= H) return;
+    const double* x = X + (int64_t)p * W;
+    double m = -INFINITY;
+    for (int t = lane; t < W; t += 32) m = fmax(m, x[t]);
+    m = warp_max(m);
+    double* e = E + (int64_t)p * W;
+    for (int t = lane; t < W; t += 32) e[t] = m == -INFINITY ? 0.0 : exp(x[t] - m);
+    if (lane == 0) M[p] = m;
+  } else {
+    // 32 columns x (blockDim / 32) row groups
+    __shared__ double part[32][33];
+    const int ng = blockDim.x >> 5;
+    const int q = blockIdx.x * 32 + lane;
+    double m = -INFINITY;
+    if (q < W)
+      for (int p = warp; p < H; p += ng) m = fmax(m, X[(int64_t)p * W + q]);
+    part[warp][lane] = m;
+    __syncthreads();
+    m = part[0][lane];
+    for (int g = 1; g < ng; ++g) m = fmax(m, part[g][lane]);
+    if (q < W) {
+      for (int p = warp; p < H; p += ng) {
+        const int64_t o = (int64_t)p * W + q;
+        E[o] = m == -INFINITY ? 0.0 : exp(X[o] - m);
+      }
+      if (warp == 0) M[q] = m;
+    }
+  }
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
-// One LSE-convolution stage as an FP64 tensor-core GEMM with the exp fused into the operand
-// load and the log into the epilogue (grid cells row-major, H x W):
-//   AX = 1:  Y[p][q] = M[p] + log sum_t exp(X[p][t] - M[p]) K[t][q]      (K = K_W, W x W)
-//   AX = 0:  Y[p][q] = M[q] + log sum_p' K[p][p'] exp(X[p'][q] - M[q])   (K = K_H, H x H)
-// M = exact max over the summed axis, computed by each CTA for its 32 rows / columns.
-// 32 x 32 output tile per CTA, 4 warps of 16 x 16 (2 x 2 DMMA m8n8k4), K staged 32 at a time
-// with a register prefetch of the next stage; padded shared strides keep fragment loads at
-// the minimum two wavefronts.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+
+// Y = Mv + log(A . B) on the FP64 tensor cores, batched over blockIdx.z; row-major
+// A (Mr x Kd), B (Kd x Nc), Y (Mr x Nc).  AX = 1: A = E_z, B = K_W, Mv_z indexed by row;
+// AX = 0: A = K_H, B = E_z, Mv_z indexed by column.  64 x 64 output tile per CTA, 4 warps of
+// 32 x 32 (4 x 4 DMMA m8n8k4), K staged 16 at a time through a 2-stage cp.async ring;
+// padded shared strides keep the fragment loads at the minimum two wavefronts.
 template <int AX>
-__global__ void __launch_bounds__(128) sep_lse_gemm_kernel(const double* __restrict__ X, const double* __restrict__ K,
-                                                           int H, int W, double* __restrict__ Y,
-                                                           const int* __restrict__ lin, int64_t xs, int64_t ys) {
+__global__ void __launch_bounds__(128) sep_gemm_log_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                           const double* __restrict__ Mv, int md, int Mr, int Nc,
+                                                           int Kd, double* __restrict__ Y, int64_t ys,
+                                                           const int* __restrict__ lin) {
   if (!*lin) return;
-  X += blockIdx.z * xs;  // batch of independent grids (blockIdx.z), one kernel matrix
+  constexpr int BM = 64, BN = 64, BK = 16, SA = BK + 4, SB = BN + 4;
+  __shared__ __align__(16) double As[2][BM * SA];
+  __shared__ __align__(16) double Bs[2][BK * SB];
+  const int64_t eo = (int64_t)blockIdx.z * Mr * Nc;  // E operand batch offset (H x W)
+  if (AX == 1) A += eo; else B += eo;
+  Mv += (int64_t)blockIdx.z * md;
   Y += blockIdx.z * ys;
-  constexpr int BT = 32, BK = 32, S = BK + 4;
-  __shared__ double As[2][BT * S];
-  __shared__ double Bs[2][BK * S];
-  __shared__ double Ms[BT];
-  __shared__ double red[4][BT];
-  const int Kd = AX == 1 ? W : H;
-  const int m0 = blockIdx.y * BT, n0 = blockIdx.x * BT;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // exact max over the summed axis for this CTA's rows (AX = 1) or columns (AX = 0)
-  if (AX == 1) {
-    for (int rr = warp; rr < BT; rr += 4) {
-      const int p = m0 + rr;
-      double m = -INFINITY;
-      if (p < H)
-        for (int t = lane; t < W; t += 32) m = fmax(m, X[(int64_t)p * W + t]);
-      m = warp_max(m);
-      if (lane == 0) Ms[rr] = m;
-    }
-  } else {
-    const int q = n0 + lane;
-    double m = -INFINITY;
-    if (q < W)
-      for (int p = warp; p < H; p += 4) m = fmax(m, X[(int64_t)p * W + q]);
-    red[warp][lane] = m;
-    __syncthreads();
-    if (warp == 0) Ms[lane] = fmax(fmax(red[0][lane], red[1][lane]), fmax(red[2][lane], red[3][lane]));
-  }
-  __syncthreads();
-  // stage loader: each thread moves 8 A and 8 B elements (rows e/32, cols e%32 of the tiles)
-  double ra[8], rb[8];
-  auto fetch = [&](int k0) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = tid + u * 128, r = e >> 5, c = e & 31;
-      // A tile: rows m0 + r, k = k0 + c;  B tile: k = k0 + r, cols n0 + c
-      const int ar = m0 + r, ak = k0 + c, bk = k0 + r, bc = n0 + c;
-      if (AX == 1) {
-        ra[u] = (ar < H && ak < Kd) ? X[(int64_t)ar * W + ak] : -INFINITY;
-        rb[u] = (bk < Kd && bc < W) ? K[(int64_t)bk * W + bc] : 0.0;
-      } else {
-        ra[u] = (ar < H && ak < Kd) ? K[(int64_t)ar * H + ak] : 0.0;
-        rb[u] = (bk < Kd && bc < W) ? X[(int64_t)bk * W + bc] : -INFINITY;
-      }
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = tid + u * 128, r = e >> 5, c = e & 31;
-      double a = ra[u], b = rb[u];
-      if (AX == 1) {
-        const double m = Ms[r];
-        a = (m == -INFINITY || a == -INFINITY) ? 0.0 : exp(a - m);
-      } else {
-        const double m = Ms[c];
-        b = (m == -INFINITY || b == -INFINITY) ? 0.0 : exp(b - m);
-      }
-      As[buf][r * S + c] = a;
-      Bs[buf][r * S + c] = b;
-    }
-  };
-  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int fr = lane >> 2, fc = lane & 3;
-  double acc[2][2][2];
+  auto stage = [&](int buf, int k0) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * 128;
+      {
+        const int r = e >> 4, c = e & 15, gr = m0 + r, gk = k0 + c;
+        const bool ok = gr < Mr && gk < Kd;
+        cp_async8(&As[buf][r * SA + c], A + (ok ? (int64_t)gr * Kd + gk : 0), ok);
+      }
+      {
+        const int r = e >> 6, c = e & 63, gk = k0 + r, gc = n0 + c;
+        const bool ok = gk < Kd && gc < Nc;
+        cp_async8(&Bs[buf][r * SB + c], B + (ok ? (int64_t)gk * Nc + gc : 0), ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][4][2];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  fetch(0);
-  store(0);
-  __syncthreads();
-  int buf = 0;
-  for (int k0 = 0; k0 < Kd; k0 += BK) {
-    const bool more = k0 + BK < Kd;
-    if (more) fetch(k0 + BK);
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nk = (Kd + BK - 1) / BK;
+  stage(0, 0);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) {
+      stage(buf ^ 1, (kt + 1) * BK);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[2], bf[2];
+      double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) af[i] = As[buf][(wm + i * 8 + fr) * S + kk + fc];
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][(wm + i * 8 + fr) * SA + kk + fc];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[buf][(kk + fc) * S + wn + j * 8 + fr];
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][(kk + fc) * SB + wn + j * 8 + fr];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    if (more) store(buf ^ 1);
     __syncthreads();
-    buf ^= 1;
   }
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int rl = wm + i * 8 + fr, row = m0 + rl;
-    if (row >= H) continue;
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm + i * 8 + fr;
+    if (row >= Mr) continue;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int cl = wn + j * 8 + 2 * fc + h, col = n0 + cl;
-        if (col >= W) continue;
-        const double mv = AX == 1 ? Ms[rl] : Ms[cl];
-        Y[(int64_t)row * W + col] = mv == -INFINITY ? -INFINITY : mv + log(acc[i][j][h]);
+        const int col = n0 + wn + j * 8 + 2 * fc + h;
+        if (col >= Nc) continue;
+        const double mv = AX == 1 ? Mv[row] : Mv[col];
+        Y[(int64_t)row * Nc + col] = mv == -INFINITY ? -INFINITY : mv + log(acc[i][j][h]);
       }
   }
 }
@@ -312,11 +326,12 @@ struct SepTab {
 };
 
 // scratch layout (doubles): 6 n-vectors, 4 tables of D, 64 spare, three (W^2 + H^2)
-// kernel-matrix slots and the three path flags
+// kernel-matrix slots, the three path flags (2 doubles), then E (n) and Mv (D) for
+// single-grid stages (batched barycenter stages place E / Mv in their own region)
 static int64_t sep_ws_doubles(const leanot_cost_t& c) {
   const int64_t D = c.height > c.width ? c.height : c.width;
   const int64_t KM = (int64_t)c.width * c.width + (int64_t)c.height * c.height;
-  return 6 * c.n + 4 * D + 3 * KM + 128;
+  return 6 * c.n + 4 * D + 3 * KM + 64 + 2 + c.n + D + 64;
 }
 
 struct SepCtx {
@@ -326,6 +341,8 @@ struct SepCtx {
   cudaStream_t st;
   int nb;
   double* K[3];
+  double* E;   // linear-domain operand, batch x n
+  double* Mv;  // its maxima, batch x max(H, W)
   int* lin;
   SepTab table(const double* a_ptr, int mode, double* g, double eta = 1.0) const {
     const int D = H > W ? H : W;
@@ -355,9 +372,15 @@ struct SepCtx {
     }
     if (xs < 0) xs = n;
     if (ys < 0) ys = n;
-    const dim3 gg((W + 31) / 32, (H + 31) / 32, nz);
-    if (ax == 1) sep_lse_gemm_kernel<1><<<gg, 128, 0, st>>>(X, t.Kw, H, W, Y, t.lin, xs, ys);
-    else sep_lse_gemm_kernel<0><<<gg, 128, 0, st>>>(X, t.Kh, H, W, Y, t.lin, xs, ys);
+    const int md = H > W ? H : W;
+    const dim3 gg((W + 63) / 64, (H + 63) / 64, nz);
+    if (ax == 1) {
+      sep_maxexp_kernel<1><<<dim3((H + 7) / 8, 1, nz), 256, 0, st>>>(X, H, W, xs, E, Mv, md, t.lin);
+      sep_gemm_log_kernel<1><<<gg, 128, 0, st>>>(E, t.Kw, Mv, md, H, W, W, Y, ys, t.lin);
+    } else {
+      sep_maxexp_kernel<0><<<dim3((W + 31) / 32, 1, nz), 1024, 0, st>>>(X, H, W, xs, E, Mv, md, t.lin);
+      sep_gemm_log_kernel<0><<<gg, 128, 0, st>>>(t.Kh, E, Mv, md, H, W, H, Y, ys, t.lin);
+    }
     sep_axis_kernel<false><<<dim3(nb, nz), 256, TAB_BYTES, st>>>(X, t.g, H, W, ax, Y, t.lin, xs, ys);
   }
   void axis_min(const double* X, const double* g, int ax, double* Y) const {
@@ -376,6 +399,8 @@ static SepCtx make_sep(const leanot_cost_t& c, cudaStream_t st, double* ws) {
   s.K[1] = s.K[0] + KM;
   s.K[2] = s.K[1] + KM;
   s.lin = reinterpret_cast<int*>(s.K[2] + KM);
+  s.E = s.K[2] + KM + 2;
+  s.Mv = s.E + c.n;
   return s;
 }
 
@@ -458,12 +483,13 @@ static bool use_sep_bary(const leanot_bary_plan_t& P) {
 // batched scratch of the barycenter plans: 4 (m x n) blocks after the separable layout
 // (barycenter.py sizes the slab as leanot_grid_sep_ws_doubles + 4 m n)
 struct BarySepWs {
-  double *Xa, *Ta, *Ya, *Ua;
+  double *Xa, *Ta, *Ya, *Ua, *E, *Mv;
 };
+// (barycenter.py sizes the slab as leanot_grid_sep_ws_doubles + 5 m n + m max(H, W))
 static BarySepWs bary_sep_ws(const leanot_bary_plan_t& P) {
   const int64_t mn = (int64_t)P.m * P.n;
   double* B = P.slab + sep_ws_doubles(P.cost);
-  return {B, B + mn, B + 2 * mn, B + 3 * mn};
+  return {B, B + mn, B + 2 * mn, B + 3 * mn, B + 4 * mn, B + 5 * mn};
 }
 
 // all 2m row log-normalizers into P.L ([w][k][i]); eval: per-k stats of weight set 0.
@@ -471,11 +497,13 @@ static BarySepWs bary_sep_ws(const leanot_bary_plan_t& P) {
 // batched launch over k.
 static int sep_bary_rows(const leanot_bary_plan_t& P, bool eval, cudaStream_t st) {
   double* ws = P.slab;
-  const SepCtx s = make_sep(P.cost, st, ws);
+  const BarySepWs B = bary_sep_ws(P);
+  SepCtx s = make_sep(P.cost, st, ws);
+  s.E = B.E;
+  s.Mv = B.Mv;
   const int64_t n = P.n, ns = P.ns;
   const int m = P.m;
   const int D = s.H > s.W ? s.H : s.W;
-  const BarySepWs B = bary_sep_ws(P);
   double *g = ws + 6 * n, *g2 = g + D;
   const int eg = s.eg(m);
   for (int w = 0; w < 2; ++w) {
@@ -503,10 +531,12 @@ static int sep_bary_rows(const leanot_bary_plan_t& P, bool eval, cudaStream_t st
 // column marginals of all (k, w) with row weights r_w (P.r, after the r-maps)
 static int sep_bary_cols(const leanot_bary_plan_t& P, cudaStream_t st) {
   double* ws = P.slab;
-  const SepCtx s = make_sep(P.cost, st, ws);
+  const BarySepWs B = bary_sep_ws(P);
+  SepCtx s = make_sep(P.cost, st, ws);
+  s.E = B.E;
+  s.Mv = B.Mv;
   const int64_t n = P.n, ns = P.ns;
   const int m = P.m;
-  const BarySepWs B = bary_sep_ws(P);
   double* g = ws + 6 * n;
   const int eg = s.eg(m);
   for (int w = 0; w < 2; ++w) {
@@ -522,11 +552,13 @@ static int sep_bary_cols(const leanot_bary_plan_t& P, cudaStream_t st) {
 
 static int sep_bary_eval(const leanot_bary_plan_t& P, cudaStream_t st) {
   double* ws = P.slab;
-  const SepCtx s = make_sep(P.cost, st, ws);
+  const BarySepWs B = bary_sep_ws(P);
+  SepCtx s = make_sep(P.cost, st, ws);
+  s.E = B.E;
+  s.Mv = B.Mv;
   const int64_t n = P.n, ns = P.ns;
   const int m = P.m;
   const int D = s.H > s.W ? s.H : s.W;
-  const BarySepWs B = bary_sep_ws(P);
   double* zero = ws + 5 * n;
   double* g3 = ws + 6 * n + 2 * D;
   cudaMemsetAsync(zero, 0, n * sizeof(double), st);

@@ -79,6 +79,8 @@ struct UpdArgs {
   double* partial;  // 2*nblk
   double* scal;     // a, a_bar, s, t
   double A, B, beta, decay, G, twosup, tau_p, tau_p_eta;
+  // batch of independent updates over blockIdx.y (barycenter marginals): element strides
+  int64_t zs_col, zs_vec;  // col / (c, ct, delta, b, bprime, b_bar, sd); partial: 2 * nblk
   int nblk;
 };
 
@@ -118,8 +120,22 @@ __device__ __forceinline__ double md_step(double A, double B, double delta, doub
   return __dadd_rn(__dmul_rn(A, delta), __ddiv_rn(__dmul_rn(B, __dsub_rn(col, c)), ct));
 }
 
+// the update of batch member blockIdx.y
+__device__ __forceinline__ UpdArgs upd_at(const UpdArgs& U0) {
+  UpdArgs U = U0;
+  const int64_t z = blockIdx.y;
+  if (z) {
+    U.col += z * U.zs_col;
+    U.c += z * U.zs_vec; U.ct += z * U.zs_vec; U.delta += z * U.zs_vec; U.b += z * U.zs_vec;
+    U.bprime += z * U.zs_vec; U.b_bar += z * U.zs_vec; U.sd += z * U.zs_vec;
+    U.partial += z * 2 * U.nblk;
+  }
+  return U;
+}
+
 // K3: mu_bar, mu_next (balanced), b' = decay*b + G*tanh(mu_bar/2)  (dxg.py:273, 277-278)
-__global__ void dxg_update1(const UpdArgs U) {
+__global__ void dxg_update1(const UpdArgs U0) {
+  const UpdArgs U = upd_at(U0);
   double mx = -INFINITY;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < U.n; j += (int64_t)gridDim.x * blockDim.x) {
     const double cj = U.c[j], ctj = U.ct[j], dj = U.delta[j];
@@ -136,7 +152,8 @@ __global__ void dxg_update1(const UpdArgs U) {
 
 // K4: b = b' - max b'; then the next midpoint weights b_bar' = decay*b + G*tanh(delta/2)
 //     and the dual shift sd = 2 sup tanh(delta/2)  (dxg.py:252, 274, 331-332)
-__global__ void dxg_update2(const UpdArgs U, int advance_scalars) {
+__global__ void dxg_update2(const UpdArgs U0, int advance_scalars) {
+  const UpdArgs U = upd_at(U0);
   const double M = max_of(U.partial, U.nblk);
   double mx = -INFINITY;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < U.n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -149,7 +166,7 @@ __global__ void dxg_update2(const UpdArgs U, int advance_scalars) {
     mx = fmax(mx, bb);
   }
   block_max_store(mx, U.partial + U.nblk + blockIdx.x);
-  if (advance_scalars && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (advance_scalars && blockIdx.x == 0 && blockIdx.y == gridDim.y - 1 && threadIdx.x == 0) {
     // TransportLogWeights(a, s, t) advance (dxg.py:253-257) and the next midpoint a
     const double a = __dadd_rn(__dmul_rn(U.decay, U.scal[0]), U.tau_p);
     U.scal[0] = a;
@@ -214,7 +231,8 @@ __global__ void __launch_bounds__(1024) dxg_update_small(const UpdArgs U) {
 }
 
 // K5: b_bar = b_bar' - max b_bar'
-__global__ void dxg_update3(const UpdArgs U) {
+__global__ void dxg_update3(const UpdArgs U0) {
+  const UpdArgs U = upd_at(U0);
   const double M = max_of(U.partial + U.nblk, U.nblk);
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < U.n; j += (int64_t)gridDim.x * blockDim.x)
     U.b_bar[j] = __dsub_rn(U.bprime[j], M);
@@ -452,6 +470,8 @@ static UpdArgs make_upd(const leanot_dxg_plan_t& P) {
   U.tau_p = q.tau_p;
   U.tau_p_eta = q.tau_p * q.eta;
   U.nblk = P.nblk_upd;
+  U.zs_col = 0;
+  U.zs_vec = 0;
   return U;
 }
 
