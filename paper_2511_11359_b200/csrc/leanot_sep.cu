@@ -606,6 +606,27 @@ int leanot_grid_sep_lse(const leanot_cost_t* cost, const double* a_dev, const do
   return check_launch("grid_sep_lse");
 }
 
+// Sinkhorn / IBP LSE on a grid: out_i = LSE_j((v_j - C_ij)/eta) (sinkhorn.py:47-71; C is
+// symmetric, so the same call gives the column LSE of (phi_i - C_ij)/eta)
+int leanot_grid_sep_lse_eta(const leanot_cost_t* cost, const double* v, double eta, double* out, double* ws,
+                            void* stream) {
+  using namespace leanot;
+  LEANOT_TRY(validate_cost(cost));
+  if (cost->kind != LEANOT_COST_GRID) { set_error("separable path needs a grid cost"); return LEANOT_EINVAL; }
+  if (!(eta > 0)) { set_error("eta must be positive"); return LEANOT_EINVAL; }
+  LEANOT_TRY(ensure_init());
+  cudaStream_t st = S_(stream);
+  const SepCtx s = make_sep(*cost, st, ws);
+  const int64_t n = cost->n;
+  const int D = s.H > s.W ? s.H : s.W;
+  double *T = ws, *X = ws + n, *g3 = ws + 6 * n + 2 * D;
+  const SepTab tg = s.table(nullptr, 3, g3, eta);          // g(d) = -f(d) inv / eta
+  sep_scale_kernel<<<s.eg(), 256, 0, st>>>(v, 1.0 / eta, n, X);
+  s.axis(X, tg, 1, T);
+  s.axis(T, tg, 0, out);
+  return check_launch("grid_sep_lse_eta");
+}
+
 int leanot_grid_sep_colsum(const leanot_cost_t* cost, const double* a_dev, const double* b, const double* logw,
                            double* col, double* ws, void* stream) {
   using namespace leanot;

@@ -11,6 +11,7 @@ one scalar (the column gap) per sweep, as the reference's stopping rule needs.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -54,7 +55,11 @@ def _torch():
 
 
 class _Sweeper:
-    """Device workspaces for row/column LSE sweeps of one kernel."""
+    """Device workspaces for row/column LSE sweeps of one kernel.
+
+    GridKernel costs take the separable O(n^1.5) path (two 1-D LSE convolutions per sweep,
+    on the FP64 tensor cores while exp(-C/eta) stays representable); C is symmetric there,
+    so the column LSE is the row LSE of the other potential."""
 
     def __init__(self, kernel):
         torch = _torch()
@@ -63,7 +68,10 @@ class _Sweeper:
         self.n = kernel.n
         self.cs = kernel.cost_struct()
         L = _lib.lib()
-        self.ws = torch.empty(int(L.leanot_col_lse_ws_doubles(self.n, self.n)), dtype=torch.float64, device=self.dev)
+        self.sep = (self.cs.kind == _lib.COST_GRID and kernel.local_rows == (0, self.n)
+                    and os.environ.get("LEANOT_GRID_SEPARABLE", "1") != "0")
+        size = L.leanot_grid_sep_ws_doubles(self.cs) if self.sep else L.leanot_col_lse_ws_doubles(self.n, self.n)
+        self.ws = torch.empty(int(size), dtype=torch.float64, device=self.dev)
 
     def vec(self, x=None):
         torch = _torch()
@@ -73,11 +81,19 @@ class _Sweeper:
 
     def row_lse(self, psi, eta, out):
         """LSE_j((psi_j - C_ij)/eta) (sinkhorn.py:65-71)."""
+        if self.sep:
+            _lib.check(_lib.lib().leanot_grid_sep_lse_eta(self.cs, psi.data_ptr(), float(eta), out.data_ptr(),
+                                                          self.ws.data_ptr(), _lib.stream_handle()), "row_lse")
+            return
         _lib.check(_lib.lib().leanot_row_lse_affine(self.cs, 0, self.n, psi.data_ptr(), -1.0, 1.0 / eta,
                                                     out.data_ptr(), _lib.stream_handle()), "row_lse")
 
     def col_lse(self, phi, eta, out):
         """LSE_i((phi_i - C_ij)/eta) (sinkhorn.py:47-62)."""
+        if self.sep:
+            _lib.check(_lib.lib().leanot_grid_sep_lse_eta(self.cs, phi.data_ptr(), float(eta), out.data_ptr(),
+                                                          self.ws.data_ptr(), _lib.stream_handle()), "col_lse")
+            return
         _lib.check(_lib.lib().leanot_col_lse(self.cs, 0, self.n, phi.data_ptr(), float(eta), out.data_ptr(),
                                              self.ws.data_ptr(), _lib.stream_handle()), "col_lse")
 

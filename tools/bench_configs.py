@@ -125,6 +125,14 @@ def config5(tte5=0.0):
     out = {"config": 5, "n": n, "m": m, "cost": "GridKernel(316,316,2): separable O(n^1.5) sweeps",
            "seconds_per_iter": per_iter, "iters_per_s": 1.0 / per_iter}
     if tte5 > 0:
+        # the IBP baseline (sinkhorn.py:174-228) on the same instance, separable sweeps
+        from paper_2511_11359_b200 import sinkhorn as SK
+        SK.ibp_barycenter(g, margs, np.full(m, 1.0 / m), 1e-3, tol=1e-9, max_iter=3)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ib = SK.ibp_barycenter(g, margs, np.full(m, 1.0 / m), 1e-3, tol=1e-9, max_iter=2000)
+        out.update({"ibp_eta": 1e-3, "ibp_seconds": time.perf_counter() - t0, "ibp_sweeps": ib.sweeps,
+                    "ibp_converged": ib.converged, "ibp_col_gap": ib.col_gap})
         t0 = time.perf_counter()
         sol = B.dxgb_solve(g, margs, np.full(m, 1.0 / m), prm, dxg.Termination(eps=1e-3, timeout=tte5), log_stride=25)
         out.update({"eps": 1e-3, "solve_seconds": time.perf_counter() - t0, "iterations": sol.iterations,
