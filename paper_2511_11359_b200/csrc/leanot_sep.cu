@@ -159,48 +159,51 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
 
 // Y = Mv + log(A . B) on the FP64 tensor cores, batched over blockIdx.z; row-major
 // A (Mr x Kd), B (Kd x Nc), Y (Mr x Nc).  AX = 1: A = E_z, B = K_W, Mv_z indexed by row;
-// AX = 0: A = K_H, B = E_z, Mv_z indexed by column.  64 x 64 output tile per CTA, 4 warps of
-// 32 x 32 (4 x 4 DMMA m8n8k4), K staged 16 at a time through a 2-stage cp.async ring;
-// padded shared strides keep the fragment loads at the minimum two wavefronts.
-template <int AX>
+// AX = 0: A = K_H, B = E_z, Mv_z indexed by column.  BT x BT output tile per CTA, 4 warps
+// of BT/2 x BT/2 (DMMA m8n8k4 tiles), K staged BK at a time through a 2-stage cp.async
+// ring; padded shared strides keep the fragment loads at the minimum two wavefronts.
+// BT = 32 for grids up to ~512 per side (enough CTAs to fill 148 SMs), 64 above.
+template <int AX, int BT>
 __global__ void __launch_bounds__(128) sep_gemm_log_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                                            const double* __restrict__ Mv, int md, int Mr, int Nc,
                                                            int Kd, double* __restrict__ Y, int64_t ys,
                                                            const int* __restrict__ lin) {
   if (!*lin) return;
-  constexpr int BM = 64, BN = 64, BK = 16, SA = BK + 4, SB = BN + 4;
-  __shared__ __align__(16) double As[2][BM * SA];
+  constexpr int BK = BT == 32 ? 32 : 16, SA = BK + 4, SB = BT + 4;
+  constexpr int WT = BT / 2, TI = WT / 8;  // warp tile, DMMA tiles per warp side
+  constexpr int LA = BT * BK / 128;         // cp.async per thread per stage and operand
+  __shared__ __align__(16) double As[2][BT * SA];
   __shared__ __align__(16) double Bs[2][BK * SB];
   const int64_t eo = (int64_t)blockIdx.z * Mr * Nc;  // E operand batch offset (H x W)
   if (AX == 1) A += eo; else B += eo;
   Mv += (int64_t)blockIdx.z * md;
   Y += blockIdx.z * ys;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.y * BT, n0 = blockIdx.x * BT;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * WT, wn = (warp & 1) * WT;
   const int fr = lane >> 2, fc = lane & 3;
   auto stage = [&](int buf, int k0) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < LA; ++u) {
       const int e = tid + u * 128;
       {
-        const int r = e >> 4, c = e & 15, gr = m0 + r, gk = k0 + c;
+        const int r = e / BK, c = e % BK, gr = m0 + r, gk = k0 + c;
         const bool ok = gr < Mr && gk < Kd;
         cp_async8(&As[buf][r * SA + c], A + (ok ? (int64_t)gr * Kd + gk : 0), ok);
       }
       {
-        const int r = e >> 6, c = e & 63, gk = k0 + r, gc = n0 + c;
+        const int r = e / BT, c = e % BT, gk = k0 + r, gc = n0 + c;
         const bool ok = gk < Kd && gc < Nc;
         cp_async8(&Bs[buf][r * SB + c], B + (ok ? (int64_t)gk * Nc + gc : 0), ok);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  double acc[4][4][2];
+  double acc[TI][TI][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < TI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int nk = (Kd + BK - 1) / BK;
   stage(0, 0);
   for (int kt = 0; kt < nk; ++kt) {
@@ -214,24 +217,24 @@ __global__ void __launch_bounds__(128) sep_gemm_log_kernel(const double* __restr
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[TI], bf[TI];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[buf][(wm + i * 8 + fr) * SA + kk + fc];
+      for (int i = 0; i < TI; ++i) af[i] = As[buf][(wm + i * 8 + fr) * SA + kk + fc];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][(kk + fc) * SB + wn + j * 8 + fr];
+      for (int j = 0; j < TI; ++j) bf[j] = Bs[buf][(kk + fc) * SB + wn + j * 8 + fr];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < TI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < TI; ++i) {
     const int row = m0 + wm + i * 8 + fr;
     if (row >= Mr) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < TI; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = n0 + wn + j * 8 + 2 * fc + h;
@@ -373,13 +376,17 @@ struct SepCtx {
     if (xs < 0) xs = n;
     if (ys < 0) ys = n;
     const int md = H > W ? H : W;
-    const dim3 gg((W + 63) / 64, (H + 63) / 64, nz);
+    const bool small = (int64_t)((W + 63) / 64) * ((H + 63) / 64) * nz < 2 * (int64_t)num_sms();
+    const int bt = small ? 32 : 64;
+    const dim3 gg((W + bt - 1) / bt, (H + bt - 1) / bt, nz);
     if (ax == 1) {
       sep_maxexp_kernel<1><<<dim3((H + 7) / 8, 1, nz), 256, 0, st>>>(X, H, W, xs, E, Mv, md, t.lin);
-      sep_gemm_log_kernel<1><<<gg, 128, 0, st>>>(E, t.Kw, Mv, md, H, W, W, Y, ys, t.lin);
+      if (small) sep_gemm_log_kernel<1, 32><<<gg, 128, 0, st>>>(E, t.Kw, Mv, md, H, W, W, Y, ys, t.lin);
+      else sep_gemm_log_kernel<1, 64><<<gg, 128, 0, st>>>(E, t.Kw, Mv, md, H, W, W, Y, ys, t.lin);
     } else {
       sep_maxexp_kernel<0><<<dim3((W + 31) / 32, 1, nz), 1024, 0, st>>>(X, H, W, xs, E, Mv, md, t.lin);
-      sep_gemm_log_kernel<0><<<gg, 128, 0, st>>>(t.Kh, E, Mv, md, H, W, H, Y, ys, t.lin);
+      if (small) sep_gemm_log_kernel<0, 32><<<gg, 128, 0, st>>>(t.Kh, E, Mv, md, H, W, H, Y, ys, t.lin);
+      else sep_gemm_log_kernel<0, 64><<<gg, 128, 0, st>>>(t.Kh, E, Mv, md, H, W, H, Y, ys, t.lin);
     }
     sep_axis_kernel<false><<<dim3(nb, nz), 256, TAB_BYTES, st>>>(X, t.g, H, W, ax, Y, t.lin, xs, ys);
   }

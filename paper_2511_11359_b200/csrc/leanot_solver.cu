@@ -359,14 +359,14 @@ __global__ void bary_e_kernel(const double* g, int64_t n, const double* partial,
   if (threadIdx.x == 0) psum[blockIdx.x] = s;
 }
 
-// r_i /= sum of the block partial sums, added in block order by every block (deterministic)
+// r_i /= sum of the block partial sums; every block adds them with the same fixed tree
+// (strided per-thread sums, then block_sum), so all blocks divide by the identical total
 __global__ void bary_norm_kernel(double* r, int64_t n, const double* psum, int nblk) {
   __shared__ double tot;
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += psum[b];
-    tot = t;
-  }
+  double t = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) t += psum[b];
+  t = block_sum(t);
+  if (threadIdx.x == 0) tot = t;
   __syncthreads();
   const double s = tot;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -8,6 +8,7 @@
 //   lds   conflict-free LDS.64 from a lane-replicated table
 //   exp   the sweep's table exp (8 FP64 + 4 INT + 1 LDS) on register data
 //   hbm   streaming 16 B/lane reads of a 16 GB buffer
+//   l2    the same reads of a 48 MB buffer (L2-resident): separates DRAM from on-chip transport
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -148,7 +149,9 @@ int main(int argc, char** argv) {
   CK(cudaFuncSetAttribute(k_exp, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES));
   uint4* buf = nullptr;
   const int64_t bytes = 16LL << 30;
+  const int64_t l2bytes = 48LL << 20;
   if (!strcmp(mode, "hbm")) CK(cudaMalloc(&buf, bytes));
+  if (!strcmp(mode, "l2")) CK(cudaMalloc(&buf, l2bytes));
   const int blocks = sms * 2, threads = 512;
   const int iters = 20000;
   double ops_per_launch = 0;  // thread-level operations of the named class
@@ -159,6 +162,10 @@ int main(int argc, char** argv) {
     else if (!strcmp(mode, "lds")) { k_lds<<<blocks, threads, TAB_BYTES>>>(out, iters); ops_per_launch = 8.0 * iters; }
     else if (!strcmp(mode, "exp")) { k_exp<<<blocks, threads, TAB_BYTES>>>(out, iters / 4, -300.0, -1.0); ops_per_launch = 8.0 * iters / 4; }
     else if (!strcmp(mode, "hbm")) { k_hbm<<<sms * 4, 512>>>(buf, bytes / 16, out); ops_per_launch = (double)bytes / ((double)blocks * threads); }
+    else if (!strcmp(mode, "l2")) {
+      for (int rep = 0; rep < 64; ++rep) k_hbm<<<sms * 4, 512>>>(buf, l2bytes / 16, out);
+      ops_per_launch = 64.0 * (double)l2bytes / ((double)blocks * threads);
+    }
     else { printf("unknown mode\n"); exit(2); }
   };
   launch();
