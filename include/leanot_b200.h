@@ -247,10 +247,12 @@ int64_t leanot_grid_sep_ws_doubles(const leanot_cost_t* cost);
 /* L_i = LSE_j(-(a C_ij + b_j)), a in device memory; ws >= leanot_grid_sep_ws_doubles(cost) doubles */
 int leanot_grid_sep_lse(const leanot_cost_t* cost, const double* a_dev, const double* b, double* L, double* ws,
                         void* stream);
-/* out_i = LSE_j((v_j - C_ij)/eta) -- the Sinkhorn/IBP row (and, C being symmetric, column) LSE
- * (sinkhorn.py:47-71); ws >= leanot_grid_sep_ws_doubles(cost) doubles */
-int leanot_grid_sep_lse_eta(const leanot_cost_t* cost, const double* v, double eta, double* out, double* ws,
-                            void* stream);
+/* out_z,i = LSE_j((v_z,j - C_ij)/eta) for nz potentials (rows z*vstride / z*ostride) -- the
+ * Sinkhorn/IBP row (and, C being symmetric, column) LSE (sinkhorn.py:47-71);
+ * ws >= leanot_grid_sep_lse_eta_ws_doubles(cost, nz) doubles */
+int64_t leanot_grid_sep_lse_eta_ws_doubles(const leanot_cost_t* cost, int nz);
+int leanot_grid_sep_lse_eta(const leanot_cost_t* cost, const double* v, int nz, int64_t vstride, double eta,
+                            double* out, int64_t ostride, double* ws, void* stream);
 /* col_j = exp(-b_j) sum_i exp(logw_i - a C_ij); ws >= leanot_grid_sep_ws_doubles(cost) doubles */
 int leanot_grid_sep_colsum(const leanot_cost_t* cost, const double* a_dev, const double* b, const double* logw,
                            double* col, double* ws, void* stream);

@@ -613,24 +613,35 @@ int leanot_grid_sep_lse(const leanot_cost_t* cost, const double* a_dev, const do
   return check_launch("grid_sep_lse");
 }
 
-// Sinkhorn / IBP LSE on a grid: out_i = LSE_j((v_j - C_ij)/eta) (sinkhorn.py:47-71; C is
-// symmetric, so the same call gives the column LSE of (phi_i - C_ij)/eta)
-int leanot_grid_sep_lse_eta(const leanot_cost_t* cost, const double* v, double eta, double* out, double* ws,
-                            void* stream) {
+// Sinkhorn / IBP LSE on a grid, for nz potentials at once (IBP: one per marginal):
+//   out_z,i = LSE_j((v_z,j - C_ij)/eta)    (sinkhorn.py:47-71)
+// C is symmetric, so the same call gives the column LSEs of (phi_i - C_ij)/eta.
+int64_t leanot_grid_sep_lse_eta_ws_doubles(const leanot_cost_t* cost, int nz) {
+  const int64_t D = cost->height > cost->width ? cost->height : cost->width;
+  return leanot::sep_ws_doubles(*cost) + (int64_t)nz * (3 * cost->n + D);
+}
+
+int leanot_grid_sep_lse_eta(const leanot_cost_t* cost, const double* v, int nz, int64_t vstride, double eta,
+                            double* out, int64_t ostride, double* ws, void* stream) {
   using namespace leanot;
   LEANOT_TRY(validate_cost(cost));
   if (cost->kind != LEANOT_COST_GRID) { set_error("separable path needs a grid cost"); return LEANOT_EINVAL; }
   if (!(eta > 0)) { set_error("eta must be positive"); return LEANOT_EINVAL; }
+  if (nz < 1 || vstride < cost->n || ostride < cost->n) { set_error("bad batch layout"); return LEANOT_EINVAL; }
   LEANOT_TRY(ensure_init());
   cudaStream_t st = S_(stream);
-  const SepCtx s = make_sep(*cost, st, ws);
+  SepCtx s = make_sep(*cost, st, ws);
   const int64_t n = cost->n;
   const int D = s.H > s.W ? s.H : s.W;
-  double *T = ws, *X = ws + n, *g3 = ws + 6 * n + 2 * D;
+  double* B = ws + sep_ws_doubles(*cost);
+  double *X = B, *T = B + nz * n;
+  s.E = B + 2 * nz * n;
+  s.Mv = B + 3 * nz * n;
+  double* g3 = ws + 6 * n + 2 * D;
   const SepTab tg = s.table(nullptr, 3, g3, eta);          // g(d) = -f(d) inv / eta
-  sep_scale_kernel<<<s.eg(), 256, 0, st>>>(v, 1.0 / eta, n, X);
-  s.axis(X, tg, 1, T);
-  s.axis(T, tg, 0, out);
+  sep_scale_kernel<<<s.eg(nz), 256, 0, st>>>(v, 1.0 / eta, n, X, nz, vstride, n);
+  s.axis(X, tg, 1, T, nz);
+  s.axis(T, tg, 0, out, nz, n, ostride);
   return check_launch("grid_sep_lse_eta");
 }
 

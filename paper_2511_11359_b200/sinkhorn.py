@@ -61,7 +61,7 @@ class _Sweeper:
     on the FP64 tensor cores while exp(-C/eta) stays representable); C is symmetric there,
     so the column LSE is the row LSE of the other potential."""
 
-    def __init__(self, kernel):
+    def __init__(self, kernel, batch: int = 1):
         torch = _torch()
         self.k = kernel
         self.dev = kernel.device
@@ -70,7 +70,9 @@ class _Sweeper:
         L = _lib.lib()
         self.sep = (self.cs.kind == _lib.COST_GRID and kernel.local_rows == (0, self.n)
                     and os.environ.get("LEANOT_GRID_SEPARABLE", "1") != "0")
-        size = L.leanot_grid_sep_ws_doubles(self.cs) if self.sep else L.leanot_col_lse_ws_doubles(self.n, self.n)
+        self.batch = int(batch)
+        size = (L.leanot_grid_sep_lse_eta_ws_doubles(self.cs, self.batch) if self.sep
+                else L.leanot_col_lse_ws_doubles(self.n, self.n))
         self.ws = torch.empty(int(size), dtype=torch.float64, device=self.dev)
 
     def vec(self, x=None):
@@ -82,8 +84,7 @@ class _Sweeper:
     def row_lse(self, psi, eta, out):
         """LSE_j((psi_j - C_ij)/eta) (sinkhorn.py:65-71)."""
         if self.sep:
-            _lib.check(_lib.lib().leanot_grid_sep_lse_eta(self.cs, psi.data_ptr(), float(eta), out.data_ptr(),
-                                                          self.ws.data_ptr(), _lib.stream_handle()), "row_lse")
+            self._sep_lse(psi, 1, eta, out)
             return
         _lib.check(_lib.lib().leanot_row_lse_affine(self.cs, 0, self.n, psi.data_ptr(), -1.0, 1.0 / eta,
                                                     out.data_ptr(), _lib.stream_handle()), "row_lse")
@@ -91,11 +92,32 @@ class _Sweeper:
     def col_lse(self, phi, eta, out):
         """LSE_i((phi_i - C_ij)/eta) (sinkhorn.py:47-62)."""
         if self.sep:
-            _lib.check(_lib.lib().leanot_grid_sep_lse_eta(self.cs, phi.data_ptr(), float(eta), out.data_ptr(),
-                                                          self.ws.data_ptr(), _lib.stream_handle()), "col_lse")
+            self._sep_lse(phi, 1, eta, out)
             return
         _lib.check(_lib.lib().leanot_col_lse(self.cs, 0, self.n, phi.data_ptr(), float(eta), out.data_ptr(),
                                              self.ws.data_ptr(), _lib.stream_handle()), "col_lse")
+
+    def _sep_lse(self, v, nz, eta, out):
+        """LSE_j((v_z,j - C_ij)/eta) for nz contiguous potentials (separable grid sweep)."""
+        _lib.check(_lib.lib().leanot_grid_sep_lse_eta(self.cs, v.data_ptr(), int(nz), self.n, float(eta),
+                                                      out.data_ptr(), self.n, self.ws.data_ptr(),
+                                                      _lib.stream_handle()), "grid_sep_lse_eta")
+
+    def row_lse_all(self, V, eta, OUT):
+        """row_lse of every row of V (m x n, contiguous) into OUT (m x n)."""
+        if self.sep and V.shape[0] <= self.batch:
+            self._sep_lse(V, V.shape[0], eta, OUT)
+            return
+        for k in range(V.shape[0]):
+            self.row_lse(V[k], eta, OUT[k])
+
+    def col_lse_all(self, V, eta, OUT):
+        """col_lse of every row of V (m x n, contiguous) into OUT (m x n)."""
+        if self.sep and V.shape[0] <= self.batch:
+            self._sep_lse(V, V.shape[0], eta, OUT)   # C symmetric on a grid
+            return
+        for k in range(V.shape[0]):
+            self.col_lse(V[k], eta, OUT[k])
 
 
 def _centered(pot: DualPotentials) -> DualPotentials:
@@ -212,7 +234,7 @@ def ibp_barycenter(kernel, marginals, weights, eta: float, tol: float = 1e-9, ma
     L = _lib.lib()
     dev = kernel.device
     with torch.cuda.device(dev):
-        sw = _Sweeper(kernel)
+        sw = _Sweeper(kernel, batch=m)
         cts = [sw.vec(ck) for ck in Ms]
         phis = torch.zeros((m, n), dtype=torch.float64, device=dev)
         psis = torch.zeros((m, n), dtype=torch.float64, device=dev)
@@ -220,22 +242,21 @@ def ibp_barycenter(kernel, marginals, weights, eta: float, tol: float = 1e-9, ma
         RL = torch.zeros((m, n), dtype=torch.float64, device=dev)
         log_r = torch.full((n,), -float(np.log(n)), dtype=torch.float64, device=dev)
         wt = sw.vec(w)
-        lcol = sw.vec()
+        LC = torch.zeros((m, n), dtype=torch.float64, device=dev)
         gaps_t = torch.zeros(m, dtype=torch.float64, device=dev)
         s = _lib.stream_handle()
         gap, converged, sweeps = np.inf, False, 0
         for sweeps in range(1, max_iter + 1):
+            sw.col_lse_all(phis, eta, LC)
             for k in range(m):
-                sw.col_lse(phis[k], eta, lcol)
-                _lib.check(L.leanot_sinkhorn_psi(cts[k].data_ptr(), lcol.data_ptr(), psis[k].data_ptr(), float(eta),
+                _lib.check(L.leanot_sinkhorn_psi(cts[k].data_ptr(), LC[k].data_ptr(), psis[k].data_ptr(), float(eta),
                                                  n, psis_new[k].data_ptr(), gaps_t[k:].data_ptr(), s), "psi")
             gap = float(gaps_t.max().item())
             if sweeps > 1 and gap <= tol:
                 converged = True
                 break
             psis, psis_new = psis_new, psis
-            for k in range(m):
-                sw.row_lse(psis[k], eta, RL[k])
+            sw.row_lse_all(psis, eta, RL)
             _lib.check(L.leanot_ibp_rows(wt.data_ptr(), m, n, float(eta), RL.data_ptr(), phis.data_ptr(),
                                          log_r.data_ptr(), s), "ibp_rows")
         lr = log_r.cpu().numpy()
