@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define LEANOT_ABI_VERSION 1
+#define LEANOT_ABI_VERSION 2
 
 #define LEANOT_OK 0
 #define LEANOT_EINVAL (-1)
@@ -55,6 +55,10 @@ typedef struct leanot_cost {
   const double* grid_coords;  /* GRID: [row index (n) | column index (n)] as doubles */
   double inv_scale;   /* 1/scale for on-the-fly kinds */
   double sup_norm;    /* ||C||_inf after normalization: 1 or 0 */
+  const double* norms;/* POINTS, p = 2, optional: |f_j|^2 (leanot_points_norms).  When set, the
+                       * non-evaluation DXG sweeps use the expanded form
+                       * a C_ij = a inv (|f_i|^2 + |f_j|^2 - 2 f_i.f_j), whose row constant
+                       * cancels in the row softmax (dxg.py:199-202) */
 } leanot_cost_t;
 
 /* K weight sets {a_k, b_k}: rows softmax_j(-(a_k C_ij + b_kj)) (dxg.py:185-190).
@@ -100,6 +104,7 @@ typedef struct leanot_dxg_plan {
   double* partial;      /* 2*nblk_upd block maxima */
   double* evalbuf;      /* 16 evaluation scalars */
   int32_t* flags;       /* 2 + 2*nr fixup list (count, -, entries) */
+  double* beta;         /* 2*((n+1)&~1) scratch for expanded-form sweeps (cost.norms set); may be null */
 } leanot_dxg_plan_t;
 
 /* ---- library ---------------------------------------------------------- */
@@ -118,6 +123,8 @@ int leanot_stored_max(const double* mat, int64_t rows, int64_t cols, int64_t ld,
 int leanot_stored_normalize(double* mat, int64_t rows, int64_t cols, int64_t ld, double scale, void* stream);
 /* raw sup over all pairs of ||f_i - f_j||_p^p (ColorKernel scale, core.py:279-284) */
 int leanot_points_sup(const double* feat, int64_t n, int dim, int p, double* out, double* scratch, void* stream);
+/* out[j] = |f_j|^2 (fma chain over the dim features): leanot_cost_t.norms of a POINTS p = 2 cost */
+int leanot_points_norms(const double* feat, int64_t n, int dim, double* out, void* stream);
 /* benchmark instance: C_ij = splitmix64(seed,i,j) -> U[0,1), C[0][n-1] = 1 (oracle/leanot_oracle.py:hash_u01) */
 int leanot_hash_fill(double* mat, int64_t row0, int64_t rows, int64_t n, int64_t ld, uint64_t seed, void* stream);
 

@@ -24,7 +24,8 @@ class CostT(C.Structure):
     _fields_ = [("kind", C.c_int32), ("p", C.c_int32), ("dim", C.c_int32), ("height", C.c_int32),
                 ("width", C.c_int32), ("_pad", C.c_int32), ("n", C.c_int64), ("ld", C.c_int64),
                 ("row_base", C.c_int64), ("mat", C.c_void_p), ("feat", C.c_void_p),
-                ("grid_coords", C.c_void_p), ("inv_scale", C.c_double), ("sup_norm", C.c_double)]
+                ("grid_coords", C.c_void_p), ("inv_scale", C.c_double), ("sup_norm", C.c_double),
+                ("norms", C.c_void_p)]
 
 
 class WsetsT(C.Structure):
@@ -41,7 +42,7 @@ class DxgPlanT(C.Structure):
                 ("row1", C.c_int64), ("splits", C.c_int32), ("nblk_upd", C.c_int32)] + [
         (name, C.c_void_p) for name in (
             "r", "c", "c_tilde", "delta", "b", "b_bar", "bprime", "sd", "scal", "shift", "m", "S",
-            "coef", "rowstat", "slab", "col", "partial", "evalbuf", "flags")]
+            "coef", "rowstat", "slab", "col", "partial", "evalbuf", "flags", "beta")]
 
 
 class BaryPlanT(C.Structure):
@@ -74,6 +75,7 @@ def lib():
         "leanot_stored_max": ([vp, i64, i64, i64, vp, vp, vp], C.c_int),
         "leanot_stored_normalize": ([vp, i64, i64, i64, dbl, vp], C.c_int),
         "leanot_points_sup": ([vp, i64, C.c_int, C.c_int, vp, vp, vp], C.c_int),
+        "leanot_points_norms": ([vp, i64, C.c_int, vp, vp], C.c_int),
         "leanot_hash_fill": ([vp, i64, i64, i64, i64, C.c_uint64, vp], C.c_int),
         "leanot_sweep_ws_doubles": ([i64, i64, C.c_int], i64),
         "leanot_column_marginals": ([C.POINTER(CostT), i64, i64, C.POINTER(WsetsT), vp, vp, vp, vp], C.c_int),
@@ -121,7 +123,7 @@ def lib():
 
 EXPORTS = (
     "leanot_version", "leanot_last_error", "leanot_device_sm_count", "leanot_dxg_default_splits",
-    "leanot_cost_block", "leanot_stored_max", "leanot_stored_normalize", "leanot_points_sup",
+    "leanot_cost_block", "leanot_stored_max", "leanot_stored_normalize", "leanot_points_sup", "leanot_points_norms",
     "leanot_hash_fill", "leanot_sweep_ws_doubles", "leanot_column_marginals", "leanot_row_lse",
     "leanot_plan_stats", "leanot_row_min", "leanot_row_lse_affine", "leanot_dxg_prepare",
     "leanot_dxg_sweep", "leanot_dxg_update", "leanot_dxg_eval", "leanot_dxg_iterate",

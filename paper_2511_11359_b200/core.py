@@ -281,6 +281,13 @@ class ColorKernel(CostKernel):
             raw_sup = float(scale)
         self.scale = raw_sup if raw_sup > 0 else 1.0
         self.sup_norm = 1.0 if raw_sup > 0 else 0.0
+        self.norms_dev = None
+        if self.p == 2:  # |f_j|^2 for the expanded-form sweeps (leanot_cost_t.norms)
+            self.norms_dev = torch.empty(self.n, dtype=torch.float64, device=self.device)
+            with torch.cuda.device(self.device):
+                _lib.check(_lib.lib().leanot_points_norms(self.features_dev.data_ptr(), self.n, self.dim,
+                                                          self.norms_dev.data_ptr(), _lib.stream_handle()),
+                           "points_norms")
 
     @property
     def features(self) -> np.ndarray:
@@ -289,7 +296,8 @@ class ColorKernel(CostKernel):
     def cost_struct(self) -> _lib.CostT:
         return _lib.CostT(kind=_lib.COST_POINTS, p=self.p, dim=self.dim, n=self.n,
                           feat=self.features_dev.data_ptr(), inv_scale=1.0 / self.scale,
-                          sup_norm=self.sup_norm)
+                          sup_norm=self.sup_norm,
+                          norms=self.norms_dev.data_ptr() if self.norms_dev is not None else None)
 
 
 def as_device_kernel(kernel, device=None) -> CostKernel:

@@ -120,6 +120,7 @@ struct CostView {
   const double* mat;
   const double* feat;
   const double* gcoord;  // grid: [row(n) | col(n)] as doubles
+  const double* norms;   // points, p = 2: |f_j|^2 (expanded-form sweeps), may be null
   double inv_scale;
 };
 
@@ -127,7 +128,7 @@ __host__ __device__ inline CostView make_view(const leanot_cost_t& c) {
   CostView v;
   v.kind = c.kind; v.p = c.p; v.dim = c.dim; v.height = c.height; v.width = c.width;
   v.n = c.n; v.ld = c.ld; v.row_base = c.row_base; v.mat = c.mat; v.feat = c.feat;
-  v.gcoord = c.grid_coords; v.inv_scale = c.inv_scale;
+  v.gcoord = c.grid_coords; v.norms = c.norms; v.inv_scale = c.inv_scale;
   return v;
 }
 

@@ -12,12 +12,17 @@ namespace leanot {
 // ExplicitKernel: normalized matrix stored row-major in HBM (core.py:239-261)
 struct CostStored {
   static constexpr bool kStored = true;
+  static constexpr bool kGram = false;
   const double* mat;
   int64_t ld, row_base;
   struct Row { const double* p; };
   struct Col {};
   __device__ explicit CostStored(const CostView& v) : mat(v.mat), ld(v.ld), row_base(v.row_base) {}
+  #ifdef LEANOT_DBG_WRAP
+  __device__ __forceinline__ Row row(int64_t i) const { return Row{mat + ((i - row_base) % LEANOT_DBG_WRAP) * ld}; }
+#else
   __device__ __forceinline__ Row row(int64_t i) const { return Row{mat + (i - row_base) * ld}; }
+#endif
   __device__ __forceinline__ Col col(int64_t) const { return Col{}; }
   __device__ __forceinline__ void eval2(const Row& r, const Col&, int64_t j, double& c0, double& c1) const {
     double2 v = __ldg(reinterpret_cast<const double2*>(r.p + j));
@@ -63,6 +68,7 @@ struct CostStored {
 template <int DIM, int P>
 struct CostPoints {
   static constexpr bool kStored = false;
+  static constexpr bool kGram = false;
   const double* f;
   double inv;
   int64_t n;
@@ -144,10 +150,89 @@ struct CostPoints {
   }
 };
 
+// ColorKernel with p = 2 in expanded (Gram) form, for the non-evaluation DXG sweeps:
+//   a C_ij = a inv (N_i + N_j - 2 f_i.f_j),   N_j = |f_j|^2  (cost.norms)
+// The row term -a inv N_i is constant along row i and cancels in the row softmax
+// (dxg.py:199-202), so the sweeps evaluate
+//   x'_kij = s_k (f_i.f_j) + beta_kj,  s_k = 2 a_k inv,  beta_kj = -a_k inv N_j - b_kj
+// and keep the row shifts in the x' convention (shift - round(-a_k inv N_i / LSTEP)).
+// Per element this is DIM FP64 for the dot product (shared by all weight sets) + 1 per
+// set, instead of 2 DIM + 1 for the difference form + 1 per set.  The value the
+// accessors return is the dot product f_i.f_j; beta_kj is precomputed once per sweep
+// (gram_beta_kernel) and read where the difference form reads b_kj.
+template <int DIM>
+struct CostGram {
+  static constexpr bool kStored = false;
+  static constexpr bool kGram = true;
+  const double* f;
+  const double* nrm;
+  double inv;
+  int64_t n;
+  struct Row { double v[DIM]; };
+  struct Col { double v0[DIM], v1[DIM]; };
+  __device__ explicit CostGram(const CostView& v) : f(v.feat), nrm(v.norms), inv(v.inv_scale), n(v.n) {}
+  __device__ __forceinline__ Row row(int64_t i) const {
+    Row r;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) r.v[d] = __ldg(f + i * DIM + d);
+    return r;
+  }
+  __device__ __forceinline__ double norm(int64_t j) const { return __ldg(nrm + j); }
+  __device__ __forceinline__ Col col(int64_t j) const {
+    Col c;
+    int64_t j1 = j + 1 < n ? j + 1 : j;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) { c.v0[d] = __ldg(f + j * DIM + d); c.v1[d] = __ldg(f + j1 * DIM + d); }
+    return c;
+  }
+  __device__ __forceinline__ static double dot(const double* a, const double* b) {
+    double s = a[0] * b[0];
+#pragma unroll
+    for (int d = 1; d < DIM; ++d) s = fma(a[d], b[d], s);
+    return s;
+  }
+  __device__ __forceinline__ double eval1(const Row& r, int64_t j) const {
+    double b[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) b[d] = __ldg(f + j * DIM + d);
+    return dot(r.v, b);
+  }
+  template <int R> struct Pre2 { Col c; };
+  template <int R>
+  __device__ __forceinline__ void pre2(const Row (&)[R], const Col&, int64_t j, Pre2<R>& p) const { p.c = col(j); }
+  template <int R>
+  __device__ __forceinline__ void get2(const Row (&rows)[R], const Col&, const Pre2<R>& p, double (&c)[R][2]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) { c[r][0] = dot(rows[r].v, p.c.v0); c[r][1] = dot(rows[r].v, p.c.v1); }
+  }
+  struct Pre4 { Row r; };
+  __device__ __forceinline__ void pre4(const Row& row, int64_t, Pre4& p) const { p.r = row; }
+  struct Col4 { double v[4][DIM]; };
+  __device__ __forceinline__ Col4 col4(int64_t j) const {
+    Col4 c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int64_t jj = j + q < n ? j + q : n - 1;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) c.v[q][d] = __ldg(f + jj * DIM + d);
+    }
+    return c;
+  }
+  __device__ __forceinline__ void eval4(const Row& r, const Col4& cl, int64_t, double* c) const {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = dot(r.v, cl.v[q]);
+  }
+  __device__ __forceinline__ void get4(const Pre4& p, const Col4& cl, double* c) const {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = dot(p.r.v, cl.v[q]);
+  }
+};
+
 // GridKernel: (|drow|^P + |dcol|^P) / scale, cells row-major (core.py:200-236)
 template <int P>
 struct CostGrid {
   static constexpr bool kStored = false;
+  static constexpr bool kGram = false;
   const double* rc;  // [row(n) | col(n)]
   double inv;
   int64_t n;

@@ -26,6 +26,7 @@ struct RowPassArgs {
   int64_t* shift_next;         // nr (may be null)
   int next_from_k;
   int32_t* flags;              // [count, -, (k, li)...]
+  int gram;                    // 1: points p = 2 with norms -> expanded-form sweep (CostGram)
 };
 
 struct ColPassArgs {
@@ -37,9 +38,11 @@ struct ColPassArgs {
   const double* coef;          // K x nr x 4
   double* slab;                // splits x K x n
   int splits;
+  int gram;                    // must match the pass A that produced m / coef
 };
 
 int num_sms();
+bool gram_enabled();
 int launch_rowpass(const RowPassArgs& A, int K, bool eval, cudaStream_t st);
 int launch_rowmax(const RowPassArgs& A, int K, int64_t* out, cudaStream_t st);
 int launch_colpass(const ColPassArgs& A, int K, cudaStream_t st);

@@ -438,6 +438,26 @@ __global__ void hash_fill_kernel(double* mat, int64_t row0, int64_t rows, int64_
   }
 }
 
+// beta_kj = -a_k inv N_j - b_kj for the expanded-form sweeps (CostGram), k = 0 (b), 1 (b_bar)
+__global__ void gram_beta_kernel(int64_t n, int64_t ld, const double* scal, double inv, const double* N,
+                                 const double* b, const double* bb, double* beta) {
+  const double na0 = (-scal[0]) * inv, na1 = (-scal[1]) * inv;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double Nj = N[j];
+    beta[j] = fma(na0, Nj, -b[j]);
+    beta[ld + j] = fma(na1, Nj, -bb[j]);
+  }
+}
+
+// |f_j|^2 for the expanded (Gram) form of squared-Euclidean costs
+__global__ void points_norms_kernel(const double* f, int64_t n, int dim, double* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = f[j * dim] * f[j * dim];
+    for (int d = 1; d < dim; ++d) s = fma(f[j * dim + d], f[j * dim + d], s);
+    out[j] = s;
+  }
+}
+
 __global__ void points_sup_kernel(const double* f, int64_t n, int dim, int p, double* partial) {
   double mx = 0.0;
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
@@ -599,6 +619,13 @@ int leanot_points_sup(const double* feat, int64_t n, int dim, int p, double* out
   points_sup_kernel<<<grid, 256, 0, S_(stream)>>>(feat, n, dim, p, scratch);
   reduce_max_kernel<<<1, 1024, 0, S_(stream)>>>(scratch, grid, out);
   return check_launch("points_sup");
+}
+
+int leanot_points_norms(const double* feat, int64_t n, int dim, double* out, void* stream) {
+  LEANOT_TRY(ensure_init());
+  if (!feat || !out || n < 1 || dim < 1 || dim > 4) { set_error("points_norms: bad arguments"); return LEANOT_EINVAL; }
+  points_norms_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, S_(stream)>>>(feat, n, dim, out);
+  return check_launch("points_norms");
 }
 
 int leanot_hash_fill(double* mat, int64_t row0, int64_t rows, int64_t n, int64_t ld, uint64_t seed, void* stream) {
@@ -791,13 +818,26 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
     return check_launch("dxg_sweep(separable)");
   }
   RowPassArgs A = make_rowpass(*P);
-  if (!(flags & LEANOT_SWEEP_COLS_ONLY)) LEANOT_TRY(launch_rowpass(A, 2, (flags & LEANOT_SWEEP_EVAL) != 0, st));
+  // squared-Euclidean points: expanded form for the plain iteration sweeps (the evaluation
+  // sweep needs C itself); pass A and pass B must agree (shift / coefficient convention)
+  const bool eval = (flags & LEANOT_SWEEP_EVAL) != 0;
+  const bool gram = !eval && P->beta && P->cost.kind == LEANOT_COST_POINTS && P->cost.p == 2 && P->cost.norms &&
+                    gram_enabled();
+  if (gram) {
+    A.gram = 1;
+    const int64_t ld = (P->n + 1) & ~int64_t(1);  // beta_1 16-byte aligned (pass A reads double2)
+    A.b[0] = P->beta; A.b[1] = P->beta + ld;
+    if (!(flags & LEANOT_SWEEP_COLS_ONLY))
+      gram_beta_kernel<<<(int)std::min<int64_t>((P->n + 255) / 256, 2048), 256, 0, st>>>(
+          P->n, ld, P->scal, P->cost.inv_scale, P->cost.norms, P->b, P->b_bar, P->beta);
+  }
+  if (!(flags & LEANOT_SWEEP_COLS_ONLY)) LEANOT_TRY(launch_rowpass(A, 2, eval, st));
   if (flags & LEANOT_SWEEP_ROWS_ONLY) return check_launch("dxg_sweep(rows)");
   ColPassArgs B;
   memset(&B, 0, sizeof(B));
   B.cost = A.cost; B.i0 = P->row0; B.i1 = P->row1; B.a = P->scal;
-  B.b[0] = P->b; B.b[1] = P->b_bar;
-  B.m = P->m; B.coef = P->coef; B.slab = P->slab; B.splits = P->splits;
+  B.b[0] = A.b[0]; B.b[1] = A.b[1];
+  B.m = P->m; B.coef = P->coef; B.slab = P->slab; B.splits = P->splits; B.gram = A.gram;
   LEANOT_TRY(launch_colpass(B, 2, st));
   LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, P->n, P->col, st));
   return check_launch("dxg_sweep");

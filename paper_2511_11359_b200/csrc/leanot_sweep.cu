@@ -44,10 +44,19 @@ constexpr int CP_CHUNK = 128;            // rows staged per smem chunk
 // log-normalizer: the row is recomputed with an exact max shift (fixup_kernel).
 __device__ __forceinline__ bool sum_ok(double S) { return S >= 0x1p-900 && S <= 0x1p900; }
 
-__device__ __forceinline__ void finalize_row(const RowPassArgs& A, int k, int64_t li, double S, int64_t m) {
+// Integer part (units of LSTEP) of the row term -a_k inv N_i that the expanded form
+// drops (CostGram); identical expression wherever it is evaluated.
+__device__ __forceinline__ int64_t gram_off(double a_k, double inv, double N_i) {
+  return llrint(((-a_k) * inv) * N_i * (1.0 / LSTEP));
+}
+
+// m: the row shift in the x convention (shift_next derives from it); mu: the shift the
+// sweep actually used, stored for pass B (mu = m except for the expanded form).
+__device__ __forceinline__ void finalize_row(const RowPassArgs& A, int k, int64_t li, double S, int64_t m,
+                                             int64_t mu) {
   const int64_t nr = A.i1 - A.i0;
   A.S[k * nr + li] = S;
-  if (A.m_used) A.m_used[k * nr + li] = m;
+  if (A.m_used) A.m_used[k * nr + li] = mu;
   if (!sum_ok(S)) {
     int slot = atomicAdd(A.flags, 1);
     A.flags[2 + 2 * slot] = k;
@@ -75,9 +84,12 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
   const int64_t nr = A.i1 - A.i0;
   const int64_t nblk = (nr + R - 1) / R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double na[K];
+  static_assert(!(EVAL && COST::kGram), "evaluation sweeps need C itself");
+  // x = mult_k * c + nb_kj: c = C_ij, mult = -a_k, nb = -b_kj; expanded form (CostGram):
+  // c = f_i.f_j, mult = 2 a_k inv, nb = beta_kj (A.b[k] points at beta_k)
+  double mult[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) na[k] = -A.a[k];
+  for (int k = 0; k < K; ++k) mult[k] = COST::kGram ? 2.0 * A.a[k] * A.cost.inv_scale : -A.a[k];
 
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int64_t ib = A.i0 + blk * R;
@@ -88,7 +100,11 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
       int64_t i = ib + r < A.i1 ? ib + r : A.i1 - 1;
       rows[r] = cost.row(i);
 #pragma unroll
-      for (int k = 0; k < K; ++k) mlo[r][k] = (uint32_t)A.shift[k * A.shift_kstride + (i - A.i0)];
+      for (int k = 0; k < K; ++k) {
+        int64_t sh = A.shift[k * A.shift_kstride + (i - A.i0)];
+        if constexpr (COST::kGram) sh -= gram_off(A.a[k], A.cost.inv_scale, cost.norm(i));
+        mlo[r][k] = (uint32_t)sh;
+      }
     }
     double acc[R][K];
     double U[R], V[R], mn[R];
@@ -115,13 +131,16 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
     auto compute = [&](const typename COST::template Pre2<R>& p, const double2 (&bv)[K], const double2& sdv) {
       double cc[R][2];
       cost.get2(rows, cl0, p, cc);
+      double2 nbv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) nbv[k] = COST::kGram ? bv[k] : make_double2(-bv[k].x, -bv[k].y);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double c0 = cc[r][0], c1 = cc[r][1];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const double x0 = fma(na[k], c0, -bv[k].x);
-          const double x1 = fma(na[k], c1, -bv[k].y);
+          const double x0 = fma(mult[k], c0, nbv[k].x);
+          const double x1 = fma(mult[k], c1, nbv[k].y);
           if (EVAL && k == 0) {
             const double e0 = texp(tb, x0, mlo[r][0]);
             const double e1 = texp(tb, x1, mlo[r][0]);
@@ -152,7 +171,8 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
         double c0 = cost.eval1(rows[r], j);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          double x0 = fma(na[k], c0, -__ldg(A.b[k] + j));
+          const double bj = __ldg(A.b[k] + j);
+          double x0 = fma(mult[k], c0, COST::kGram ? bj : -bj);
           double e0 = texp(tb, x0, mlo[r][k]);
           acc[r][k] += e0;
           if (EVAL && k == 0) {
@@ -189,7 +209,12 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
       if (v < R * K) {
         const int r = v / K, k = v % K;
         const int64_t i = ib + r;
-        if (i < A.i1) finalize_row(A, k, i - A.i0, t, A.shift[k * A.shift_kstride + (i - A.i0)]);
+        if (i < A.i1) {
+          const int64_t m = A.shift[k * A.shift_kstride + (i - A.i0)];
+          int64_t mu = m;
+          if constexpr (COST::kGram) mu -= gram_off(A.a[k], A.cost.inv_scale, cost.norm(i));
+          finalize_row(A, k, i - A.i0, t, m, mu);
+        }
       } else if (EVAL) {
         const int q = v - R * K, r = q / 3, s = q % 3;
         const int64_t i = ib + r;
@@ -220,9 +245,10 @@ __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
     const int64_t li = A.flags[3 + 2 * e];
     const int64_t i = A.i0 + li;
     const typename COST::Row row = cost.row(i);
-    const double na = -A.a[k];
+    const double mult = COST::kGram ? 2.0 * A.a[k] * A.cost.inv_scale : -A.a[k];
+    auto xval = [&](int64_t j) { return fma(mult, cost.eval1(row, j), COST::kGram ? A.b[k][j] : -A.b[k][j]); };
     double mx = -INFINITY;
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = fmax(mx, fma(na, cost.eval1(row, j), -A.b[k][j]));
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = fmax(mx, xval(j));
     mx = warp_max(mx);
     if (lane == 0) red[warp] = mx;
     __syncthreads();
@@ -235,8 +261,7 @@ __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
     const int64_t m = llrint(bcast * (1.0 / LSTEP));
     const uint32_t mlo = (uint32_t)m;
     double s = 0.0;
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
-      texp_acc(tb, fma(na, cost.eval1(row, j), -A.b[k][j]), mlo, s);
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) texp_acc(tb, xval(j), mlo, s);
     s = warp_sum(s);
     __syncthreads();
     if (lane == 0) red[warp] = s;
@@ -253,7 +278,10 @@ __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
         double* cf = A.coef + (k * nr + li) * 4;
         cf[0] = g * EC0; cf[1] = g * EC1; cf[2] = g * EC2; cf[3] = g * EC3;
       }
-      if (A.shift_next && k == A.next_from_k) A.shift_next[li] = m + llrint(log(t) * (1.0 / LSTEP));
+      // expanded form: m is in the x' convention; the stored shift is in the x convention
+      int64_t off = 0;
+      if constexpr (COST::kGram) off = gram_off(A.a[k], A.cost.inv_scale, cost.norm(i));
+      if (A.shift_next && k == A.next_from_k) A.shift_next[li] = m + off + llrint(log(t) * (1.0 / LSTEP));
     }
     __syncthreads();
   }
@@ -312,9 +340,9 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
   const int64_t ntiles = (n + CP_TILE - 1) / CP_TILE;
   const int64_t items = ntiles * A.splits;
   const int64_t rows_per_split = (nr + A.splits - 1) / A.splits;
-  double na[K];
+  double mult[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) na[k] = -A.a[k];
+  for (int k = 0; k < K; ++k) mult[k] = COST::kGram ? 2.0 * A.a[k] * A.cost.inv_scale : -A.a[k];
 
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t tile = it % ntiles, split = it / ntiles;
@@ -327,7 +355,7 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
-      for (int v = 0; v < CP_V; ++v) nb[k][v] = v < nv ? -__ldg(A.b[k] + j + v) : 0.0;
+      for (int v = 0; v < CP_V; ++v) nb[k][v] = v < nv ? (COST::kGram ? 1.0 : -1.0) * __ldg(A.b[k] + j + v) : 0.0;
     double acc[K][CP_V];
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -368,7 +396,7 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
             const uint32_t mlo = s_m[q * K + k];
 #pragma unroll
             for (int v = 0; v < CP_V; ++v)
-              texp_gacc(tb, fma(na[k], c[v], nb[k][v]), mlo, g01.x, g01.y, g23.x, g23.y, acc[k][v]);
+              texp_gacc(tb, fma(mult[k], c[v], nb[k][v]), mlo, g01.x, g01.y, g23.x, g23.y, acc[k][v]);
           }
         };
         fetch(pa0, 0);
@@ -396,7 +424,7 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
 #pragma unroll
               for (int k = 0; k < K; ++k) {
                 const double* cf = s_coef + (q * K + k) * 4;
-                texp_gacc(tb, fma(na[k], cv, nb[k][v]), s_m[q * K + k], cf[0], cf[1], cf[2], cf[3],
+                texp_gacc(tb, fma(mult[k], cv, nb[k][v]), s_m[q * K + k], cf[0], cf[1], cf[2], cf[3],
                           acc[k][v]);
               }
             }
@@ -530,6 +558,16 @@ static bool tma_enabled() {
   return v == 1;
 }
 
+// LEANOT_GRAM=0 keeps the difference form for squared-Euclidean point costs (A/B comparisons)
+bool gram_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LEANOT_GRAM");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool tma_cols_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -595,6 +633,10 @@ static int launch_fixup_t(const RowPassArgs& A, cudaStream_t st) {
   return LEANOT_OK;
 }
 
+// squared-Euclidean point costs -> their expanded-form provider (CostGram)
+template <class C> struct GramOf { using type = void; };
+template <int D> struct GramOf<CostPoints<D, 2>> { using type = CostGram<D>; };
+
 struct RowPassFn {
   const RowPassArgs& A;
   int K;
@@ -604,6 +646,17 @@ struct RowPassFn {
   int run() {
     int rc;
     constexpr int R = LEANOT_RP_R;
+    using G = typename GramOf<COST>::type;
+    if constexpr (!std::is_void<G>::value) {
+      if (!eval && A.gram && A.cost.norms) {
+        if (K == 1) rc = launch_rowpass_t<G, 1, R, false>(A, st);
+        else if (K == 2) rc = launch_rowpass_t<G, 2, R, false>(A, st);
+        else return LEANOT_EINVAL;
+        if (rc != LEANOT_OK) return rc;
+        if (A.flags) return launch_fixup_t<G>(A, st);
+        return LEANOT_OK;
+      }
+    }
     if constexpr (std::is_same<COST, CostStored>::value) {
       if (tma_ok(A.cost) && (K == 1 || K == 2)) {
         if (K == 1) rc = eval ? launch_rowpass_tma_t<1, 4, true>(A, st) : launch_rowpass_tma_t<1, 4, false>(A, st);
@@ -676,6 +729,14 @@ struct ColPassFn {
   cudaStream_t st;
   template <class COST>
   int run() {
+    using G = typename GramOf<COST>::type;
+    if constexpr (!std::is_void<G>::value) {
+      if (A.gram && A.cost.norms) {
+        if (K == 1) return launch_colpass_t<G, 1>(A, st);
+        if (K == 2) return launch_colpass_t<G, 2>(A, st);
+        return LEANOT_EINVAL;
+      }
+    }
     if constexpr (std::is_same<COST, CostStored>::value) {
       // the TMA column pass is kept for experiments (LEANOT_TMA_COLS=1); measured slower
       // than the register-pipelined one (profiles/r01_tma.md)

@@ -198,7 +198,10 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
       if (v < R * K) {
         const int r = v / K, k = v % K;
         const int64_t i = ib + r;
-        if (i < A.i1) finalize_row(A, k, i - A.i0, t, A.shift[k * A.shift_kstride + (i - A.i0)]);
+        if (i < A.i1) {
+          const int64_t m = A.shift[k * A.shift_kstride + (i - A.i0)];
+          finalize_row(A, k, i - A.i0, t, m, m);
+        }
       } else if (EVAL) {
         const int qq = v - R * K, r = qq / 3, s2 = qq % 3;
         const int64_t i = ib + r;

@@ -107,6 +107,9 @@ class DxgEngine:
         self.partial = torch.zeros(2 * nblk, **f64)
         self.evalbuf = torch.zeros(16, **f64)
         self.flags = torch.zeros(2 + 4 * nr, dtype=torch.int32, device=dev)
+        # expanded-form sweeps of squared-Euclidean points (leanot_cost_t.norms): beta_0 | beta_1,
+        # each padded to an even length
+        self.beta = torch.zeros(2 * (n + 1), **f64) if kernel.cost_struct().norms else None
         self.params = params
         self.plan = _lib.DxgPlanT()
         p = self.plan
@@ -116,6 +119,7 @@ class DxgEngine:
         for name in ("r", "c", "c_tilde", "delta", "b", "b_bar", "bprime", "sd", "scal", "shift", "m", "S",
                      "coef", "rowstat", "slab", "col", "partial", "evalbuf", "flags"):
             setattr(p, name, getattr(self, name).data_ptr())
+        p.beta = self.beta.data_ptr() if self.beta is not None else None
         self._graphs = {}
         pos = rw > 0
         self.h_r = float(-(rw[pos] * np.log(rw[pos])).sum())  # H(r) (dxg.py:308-309, 340-341)

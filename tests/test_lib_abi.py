@@ -31,17 +31,41 @@ def test_library_exports_every_declared_symbol():
 def test_version_and_error_string_without_gpu():
     from paper_2511_11359_b200 import _lib
     L = _lib.lib()
-    assert L.leanot_version() == 1
+    assert L.leanot_version() == 2
     assert isinstance(L.leanot_last_error(), bytes)
 
 
-def test_struct_layout_matches_header():
-    """ctypes mirrors must match the C layout (offsets of the last fields)."""
+def test_struct_layout_matches_header(tmp_path):
+    """ctypes mirrors must match the C layout: sizeof and every field offset, measured by
+    compiling the header with gcc."""
+    import shutil
+    import subprocess
+    import pytest
     from paper_2511_11359_b200 import _lib
-    assert ctypes.sizeof(_lib.CostT) == 4 * 6 + 8 * 3 + 8 * 3 + 8 * 2
-    assert ctypes.sizeof(_lib.WsetsT) == 8 + 8 + 8 * _lib.MAX_K
-    assert ctypes.sizeof(_lib.ParamsT) == 6 * 8
-    assert _lib.DxgPlanT.flags.offset == ctypes.sizeof(_lib.DxgPlanT) - 8
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    structs = {"leanot_cost_t": _lib.CostT, "leanot_wsets_t": _lib.WsetsT, "leanot_params_t": _lib.ParamsT,
+               "leanot_dxg_plan_t": _lib.DxgPlanT, "leanot_bary_plan_t": _lib.BaryPlanT}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{ROOT / "include" / "leanot_b200.h"}"',
+             "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            if fname.startswith("_"):
+                continue
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in structs.items():
+        assert got[(cname, "sizeof")] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            if not fname.startswith("_"):
+                assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
 
 
 def test_invalid_arguments_raise_value_error_without_gpu():
