@@ -158,6 +158,9 @@ int leanot_dxg_prepare(const leanot_dxg_plan_t* plan, double a, double s, double
 #define LEANOT_SWEEP_EVAL 1
 #define LEANOT_SWEEP_ROWS_ONLY 2
 #define LEANOT_SWEEP_COLS_ONLY 4
+/* stored cost, plain iteration: one persistent launch, pass B re-reads C from L2
+ * (csrc/leanot_fused.cu; experimental, slower than the two-pass kernels as of r01) */
+#define LEANOT_SWEEP_FUSED 8
 int leanot_dxg_sweep(const leanot_dxg_plan_t* plan, int flags, void* stream);
 /* O(n) updates after plan->col holds the (globally reduced) marginals: state <- next state */
 int leanot_dxg_update(const leanot_dxg_plan_t* plan, void* stream);

@@ -7,3 +7,4 @@
 #include "leanot_dense.cu"
 #include "leanot_sep.cu"
 #include "leanot_persist.cu"
+#include "leanot_fused.cu"

@@ -501,6 +501,9 @@ static int sep_dxg_sweep(const leanot_dxg_plan_t& P, bool eval, cudaStream_t st)
 static int sep_dxg_eval(const leanot_dxg_plan_t& P, cudaStream_t st);
 // persistent small-n iterations (leanot_persist.cu)
 static int try_persist_iterate(const leanot_dxg_plan_t& P, int iters, cudaStream_t st);
+// single-launch L2-reuse sweep for stored costs (leanot_fused.cu)
+static int try_fused_sweep(const leanot_dxg_plan_t& P, cudaStream_t st);
+static bool fused_default();
 
 // plans whose O(n) work fits one CTA and whose sweep covers all rows (single process):
 // launch-bound regime, fused update path (reduces the column slabs itself)
@@ -830,6 +833,12 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
     if (!(flags & LEANOT_SWEEP_COLS_ONLY))
       gram_beta_kernel<<<(int)std::min<int64_t>((P->n + 255) / 256, 2048), 256, 0, st>>>(
           P->n, ld, P->scal, P->cost.inv_scale, P->cost.norms, P->b, P->b_bar, P->beta);
+  }
+  if (!eval && !gram && !(flags & (LEANOT_SWEEP_ROWS_ONLY | LEANOT_SWEEP_COLS_ONLY)) &&
+      ((flags & LEANOT_SWEEP_FUSED) || fused_default())) {
+    const int rc = try_fused_sweep(*P, st);
+    if (rc == LEANOT_OK) return check_launch("dxg_sweep(fused)");
+    if (rc != LEANOT_EINVAL) return rc;
   }
   if (!(flags & LEANOT_SWEEP_COLS_ONLY)) LEANOT_TRY(launch_rowpass(A, 2, eval, st));
   if (flags & LEANOT_SWEEP_ROWS_ONLY) return check_launch("dxg_sweep(rows)");

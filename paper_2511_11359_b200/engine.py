@@ -153,10 +153,11 @@ class DxgEngine:
     def _stream(self):
         return _lib.stream_handle()
 
-    def sweep(self, evaluate=False):
+    def sweep(self, evaluate=False, fused=False):
+        """fused: stored costs only -- the experimental single-launch sweep (csrc/leanot_fused.cu)"""
+        flags = (1 if evaluate else 0) | (8 if fused else 0)
         with _torch().cuda.device(self.device):
-            _lib.check(_lib.lib().leanot_dxg_sweep(C.byref(self.plan), 1 if evaluate else 0, self._stream()),
-                       "dxg_sweep")
+            _lib.check(_lib.lib().leanot_dxg_sweep(C.byref(self.plan), flags, self._stream()), "dxg_sweep")
         if self.world > 1:
             self._combine_cols()
 
