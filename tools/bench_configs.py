@@ -95,9 +95,13 @@ def config4(shards=8):
     eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
     eng.sweep(); eng.update()
     per_iter = timed_iters(eng, 2)
-    fp64 = 2 * 2 * 8 * n * (r1 - r0) / per_iter     # two passes x two weight sets x 8 FP64 instr
+    # FP64 instructions per element and pass (expanded form, csrc/leanot_cost.cuh CostGram<3>):
+    # dot product 3 (DMUL + 2 DFMA) + per weight set: x' 1 + table exp 7 (incl. the accumulate)
+    per_elem = 2 * (3 + 2 * 8)
+    fp64 = per_elem * n * (r1 - r0) / per_iter
     return {"config": 4, "n": n, "rows_this_gpu": r1 - r0, "shards": shards, "seconds_per_iter_per_gpu": per_iter,
             "projected_iters_per_s_8gpu": 1.0 / per_iter, "fp64_instr_per_s": fp64,
+            "fp64_instr_per_element_iter": per_elem, "fp64_frac_of_measured_dfma_peak": fp64 / 17.07e12,
             "note": "1 GPU runs one 1/8 row shard; the 8-GPU run adds one 16 MB all-gather per iteration"}
 
 
