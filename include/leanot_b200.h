@@ -215,6 +215,12 @@ int leanot_bary_eval(const leanot_bary_plan_t* plan, void* stream);
  * scratch >= n + 2048 doubles */
 int leanot_bary_rmap(const double* L, int m, int64_t n, const double* w, double* r, double* scratch, void* stream);
 
+/* Multi-GPU combine of row-shard partials (column marginals, evaluation scalars): out[j] =
+ * sum over ranks q = 0..world-1 of gathered[q*count + j], added in rank order, so every rank
+ * holds bitwise-identical sums whatever the collective's internal order (the all-gather
+ * replaces the reference's in-process block sum, dxg.py:205-207).  out may alias gathered. */
+int leanot_sum_partials(const double* gathered, int world, int64_t count, double* out, void* stream);
+
 /* ---- Sinkhorn / IBP baselines (sinkhorn.py:47-228) -- */
 int64_t leanot_col_lse_ws_doubles(int64_t n, int64_t rows);
 /* L_j = LSE_i((phi_i - C_ij)/eta) over rows [row0,row1) (sinkhorn.py:47-62); row LSEs: leanot_row_lse_affine */

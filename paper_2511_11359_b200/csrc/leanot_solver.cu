@@ -438,6 +438,15 @@ __global__ void hash_fill_kernel(double* mat, int64_t row0, int64_t rows, int64_
   }
 }
 
+// out[j] = sum of the world ranks' partials in rank order (engine.combine_partials)
+__global__ void sum_partials_kernel(const double* g, int world, int64_t count, double* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = g[j];
+    for (int q = 1; q < world; ++q) s += g[(int64_t)q * count + j];
+    out[j] = s;
+  }
+}
+
 // beta_kj = -a_k inv N_j - b_kj for the expanded-form sweeps (CostGram), k = 0 (b), 1 (b_bar)
 __global__ void gram_beta_kernel(int64_t n, int64_t ld, const double* scal, double inv, const double* N,
                                  const double* b, const double* bb, double* beta) {
@@ -629,6 +638,15 @@ int leanot_points_norms(const double* feat, int64_t n, int dim, double* out, voi
   if (!feat || !out || n < 1 || dim < 1 || dim > 4) { set_error("points_norms: bad arguments"); return LEANOT_EINVAL; }
   points_norms_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, S_(stream)>>>(feat, n, dim, out);
   return check_launch("points_norms");
+}
+
+int leanot_sum_partials(const double* gathered, int world, int64_t count, double* out, void* stream) {
+  LEANOT_TRY(ensure_init());
+  if (!gathered || !out || world < 1 || count < 0) { set_error("sum_partials: bad arguments"); return LEANOT_EINVAL; }
+  if (count == 0) return LEANOT_OK;
+  sum_partials_kernel<<<(int)std::min<int64_t>((count + 255) / 256, 4096), 256, 0, S_(stream)>>>(gathered, world, count,
+                                                                                                 out);
+  return check_launch("sum_partials");
 }
 
 int leanot_hash_fill(double* mat, int64_t row0, int64_t rows, int64_t n, int64_t ld, uint64_t seed, void* stream) {

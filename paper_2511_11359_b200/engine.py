@@ -48,6 +48,14 @@ def combine_partials(local, group, world: int):
     flat = local.contiguous().view(-1)
     gathered = torch.empty(world * flat.numel(), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(gathered, flat, group=group)
+    if gathered.is_cuda:
+        # rank-order sum on the device (leanot_sum_partials)
+        out = torch.empty_like(flat)
+        with torch.cuda.device(gathered.device):
+            _lib.check(_lib.lib().leanot_sum_partials(gathered.data_ptr(), int(world), flat.numel(), out.data_ptr(),
+                                                      _lib.stream_handle()), "sum_partials")
+        return out.view(local.shape)
+    # CPU tensors: the gloo host-logic tests (tests/test_distributed_gloo.py) only
     gathered = gathered.view((world,) + tuple(local.shape))
     acc = gathered[0].clone()
     for q in range(1, world):
