@@ -109,9 +109,14 @@ def test_trajectory_per_iteration(name, scheme):
     assert [a, s, t] == d[f"{scheme}_traj_scalars"].tolist()
 
 
-@pytest.mark.parametrize("name", SOLVES)
-def test_solve_vs_reference(name):
-    """Same iteration count, same converged flag, trajectory and final cost."""
+@pytest.mark.parametrize("name", SOLVES + [s + "@graph" for s in SOLVES if "points" in s])
+def test_solve_vs_reference(name, monkeypatch):
+    """Same iteration count, same converged flag, trajectory and final cost.  "@graph": the
+    launch-per-kernel path (CUDA graph of sweeps + updates) instead of the persistent small-n
+    kernel, i.e. the expanded-form sweeps for squared-Euclidean points."""
+    if name.endswith("@graph"):
+        name = name[: -len("@graph")]
+        monkeypatch.setenv("LEANOT_PERSIST", "0")
     dxg = _dxg()
     d = load(name)
     k = device_cost(d)
