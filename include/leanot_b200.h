@@ -215,6 +215,22 @@ int leanot_bary_eval(const leanot_bary_plan_t* plan, void* stream);
  * scratch >= n + 2048 doubles */
 int leanot_bary_rmap(const double* L, int m, int64_t n, const double* w, double* r, double* scratch, void* stream);
 
+/* Row-sharded (multi-GPU) barycenter sweep, plan rows [row0,row1): three stream-ordered
+ * phases with the caller's collectives in between (the r-map normalizers and
+ * the 2 m n column partials are the only exchanges; barycenter.py:90-97, 108-151).
+ *   rows:  pass A of every marginal over the plan's rows (both weight sets), the sorted k-sum
+ *          g_w,i into r[w*n + i], gmax[w] = max of g_w over the plan's rows   (w = 0 now, 1 bar)
+ *          -> caller: gmax = max over ranks
+ *   rnorm: r_w,i = exp(g_w,i - gmax[w]), esum[w] = their sum over the plan's rows (fixed order)
+ *          -> caller: esum = rank-order sum over ranks
+ *   cols:  r_w,i /= esum[w], row coefficients, pass B of every marginal -> col (this rank's
+ *          2 m n partials) -> caller: rank-order sum (leanot_sum_partials), then leanot_bary_update
+ * gmax / esum: 2 device doubles each.  leanot_bary_eval on a sharded plan reports row sums and
+ * evalbuf[127] (LSE of the dual's g) over the plan's rows; the caller combines them. */
+int leanot_bary_rows(const leanot_bary_plan_t* plan, int flags, double* gmax, void* stream);
+int leanot_bary_rnorm(const leanot_bary_plan_t* plan, const double* gmax, double* esum, void* stream);
+int leanot_bary_cols(const leanot_bary_plan_t* plan, const double* esum, void* stream);
+
 /* Multi-GPU combine of row-shard partials (column marginals, evaluation scalars): out[j] =
  * sum over ranks q = 0..world-1 of gathered[q*count + j], added in rank order, so every rank
  * holds bitwise-identical sums whatever the collective's internal order (the all-gather

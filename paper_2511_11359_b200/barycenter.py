@@ -17,6 +17,7 @@ import numpy as np
 
 from . import _lib
 from .core import CostKernel, Histogram, as_device_kernel, as_weights
+from .engine import default_group
 from .dxg import (DxgParams, LogOddsField, Termination, TrajectoryPoint, TransportLogWeights, _plan_stats,
                   _to_dev, _ws, _wsets)
 
@@ -80,13 +81,29 @@ class BarycenterSolution:
 
 
 class BaryEngine:
-    """Device state + workspaces of one barycenter solve (single process)."""
+    """Device state + workspaces of one barycenter solve.
 
-    def __init__(self, kernel: CostKernel, marginals, w, params: DxgParams):
+    With a torch.distributed group (one process per GPU) the rows of the cost are
+    sharded (engine.shard_rows); per iteration the ranks exchange the two r-map
+    normalizers (max, then rank-order sum of the exp-sums) and the 2 m n column
+    partials (rank-order sum); the O(n) updates run redundantly.
+    """
+
+    def __init__(self, kernel: CostKernel, marginals, w, params: DxgParams, group=None):
         torch = _torch()
         self.kernel = kernel
         self.device = dev = kernel.device
         n = self.n = kernel.n
+        self.group, self.world, self.rank = group, 1, 0
+        if group is not None:
+            import torch.distributed as dist
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        r0, r1 = kernel.local_rows
+        if self.world > 1 and (r0, r1) == (0, n):
+            from .engine import shard_rows
+            r0, r1 = shard_rows(n, self.world, self.rank)
+        self.row0, self.row1 = r0, r1
+        self.sharded = (r0, r1) != (0, n)
         M = np.stack([as_weights(h) for h in marginals])
         m = self.m = M.shape[0]
         if M.shape[1] != n:
@@ -129,7 +146,9 @@ class BaryEngine:
         p = self.plan = _lib.BaryPlanT()
         p.cost = kernel.cost_struct()
         p.prm = _lib.ParamsT(params.eta, params.eta_mu, params.tau_p, params.tau_mu, params.beta, params.alpha)
-        p.n, p.row0, p.row1, p.ns, p.m, p.splits, p.nblk_upd = n, 0, n, ns, m, int(splits), nblk
+        p.n, p.row0, p.row1, p.ns, p.m, p.splits, p.nblk_upd = n, r0, r1, ns, m, int(splits), nblk
+        self.gmax = z(2)   # sharded sweeps: r-map normalizers (leanot_bary_rows / _rnorm)
+        self.esum = z(2)
         for name in ("w", "c", "c_tilde", "delta", "b", "b_bar", "bprime", "sd", "scal", "shift", "mu", "S", "L",
                      "r", "coef", "rowstat", "slab", "col", "partial", "scratch", "evalbuf", "flags"):
             setattr(p, name, getattr(self, name).data_ptr())
@@ -148,7 +167,31 @@ class BaryEngine:
         self._call("leanot_bary_prepare", float(a), float(s), float(t), 1 if fresh else 0)
 
     def sweep(self, evaluate=False):
-        self._call("leanot_bary_sweep", 1 if evaluate else 0)
+        if not self.sharded:
+            self._call("leanot_bary_sweep", 1 if evaluate else 0)
+            return
+        import torch.distributed as dist
+        from .engine import combine_partials
+        self.sweep_rows(evaluate)
+        if self.world > 1:
+            dist.all_reduce(self.gmax, op=dist.ReduceOp.MAX, group=self.group)   # order-independent
+        self.sweep_rnorm()
+        if self.world > 1:
+            self.esum.copy_(combine_partials(self.esum, self.group, self.world))
+        self.sweep_cols()
+        if self.world > 1:
+            self.col.copy_(combine_partials(self.col, self.group, self.world))
+
+    # the three phases of a row-sharded sweep (leanot_bary_rows / _rnorm / _cols); sweep()
+    # puts the collectives between them
+    def sweep_rows(self, evaluate=False):
+        self._call("leanot_bary_rows", 1 if evaluate else 0, self.gmax.data_ptr())
+
+    def sweep_rnorm(self):
+        self._call("leanot_bary_rnorm", self.gmax.data_ptr(), self.esum.data_ptr())
+
+    def sweep_cols(self):
+        self._call("leanot_bary_cols", self.esum.data_ptr())
 
     def update(self):
         self._call("leanot_bary_update")
@@ -161,11 +204,39 @@ class BaryEngine:
 
     def barycenter(self):
         """r_now of the last sweep = barycenter_marginal(state) (barycenter.py:100-105)."""
+        if self.world > 1:
+            return self._gather_rows(self.r[: self.n]).cpu().numpy()
         return self.r[: self.n].cpu().numpy()
+
+    def _combine_eval(self):
+        torch = _torch()
+        import torch.distributed as dist
+        gathered = torch.empty(self.world * self.evalbuf.numel(), dtype=torch.float64, device=self.evalbuf.device)
+        dist.all_gather_into_tensor(gathered, self.evalbuf, group=self.group)
+        bufs = gathered.view(self.world, -1).cpu().numpy()
+        self.evalbuf.copy_(torch.from_numpy(_combine_eval_buffers(bufs, self.m)))
+
+    def _gather_rows(self, full):
+        """Every rank's own rows of a length-n device vector, assembled on all ranks."""
+        torch = _torch()
+        import torch.distributed as dist
+        from .engine import shard_rows
+        per = (self.n + self.world - 1) // self.world
+        buf = torch.zeros(per, dtype=full.dtype, device=full.device)
+        buf[: self.row1 - self.row0] = full[self.row0:self.row1]
+        out = torch.empty(per * self.world, dtype=full.dtype, device=full.device)
+        dist.all_gather_into_tensor(out, buf, group=self.group)
+        res = torch.empty_like(full)
+        for q in range(self.world):
+            a, b = shard_rows(self.n, self.world, q)
+            res[a:b] = out[q * per: q * per + (b - a)]
+        return res
 
     def evaluate(self):
         """(primal, dual, infeas[m]) of the state swept by the last sweep(evaluate=True)."""
         self._call("leanot_bary_eval")
+        if self.world > 1:
+            self._combine_eval()
         buf = self.evalbuf.cpu().numpy()
         eta, sup = self.params.eta, self.kernel.sup_norm
         r = self.barycenter()
@@ -182,6 +253,26 @@ class BaryEngine:
             lead += self.wv[k] * (-2.0 * sup * cd_k)                                # barycenter.py:192
         dual = lead - eta * float(buf[127])                                         # barycenter.py:195
         return primal, dual, infeas
+
+
+def _combine_eval_buffers(bufs, m):
+    """Rank-order combination of per-rank evaluation buffers (sharded plans): row sums
+    [4k], [4k+1] add; column stats [64+2k], [65+2k] are identical on every rank; [127] is a
+    log-sum-exp over each rank's rows: M + log(sum_q exp(l_q - M)), q in rank order."""
+    out = np.array(bufs[0], dtype=float)
+    for k in range(m):
+        for j in (4 * k, 4 * k + 1):
+            v = bufs[0][j]
+            for q in range(1, len(bufs)):
+                v += bufs[q][j]
+            out[j] = v
+    ls = [float(b[127]) for b in bufs]
+    M = max(ls)
+    tot = 0.0
+    for v in ls:
+        tot += float(np.exp(v - M))
+    out[127] = M + float(np.log(tot))
+    return out
 
 
 def _log_normalizers(a: float, bs: np.ndarray, kernel: CostKernel, workers: int = 1) -> np.ndarray:
@@ -232,7 +323,7 @@ def dxgb_step(state: BarycenterState, kernel: CostKernel, marginals, params: Dxg
     if len(marginals) != m or kernel.n != n:
         raise ValueError("state/marginal/kernel size mismatch")
     kernel = as_device_kernel(kernel)
-    eng = BaryEngine(kernel, marginals, state.w, params)
+    eng = BaryEngine(kernel, marginals, state.w, params, group=default_group())
     eng.load_state(state.deltas, state.bs, state.a, state.s, state.t, fresh=False)
     eng.sweep()
     eng.update()
@@ -263,7 +354,7 @@ def dxgb_solve(kernel: CostKernel, marginals, w, params: DxgParams, termination:
     kernel = as_device_kernel(kernel)
     torch = _torch()
     state0 = BarycenterState.initial(kernel.n, w, params.eta)
-    eng = BaryEngine(kernel, marginals, state0.w, params)
+    eng = BaryEngine(kernel, marginals, state0.w, params, group=default_group())
     eng.load_state(state0.deltas, state0.bs, 0.0, 0.0, 0, fresh=True)
     t0 = time.perf_counter()
     trajectory: list[TrajectoryPoint] = []

@@ -75,10 +75,9 @@ static int sep_bary_eval(const leanot_bary_plan_t& P, cudaStream_t st);
 static int validate_bary(const leanot_bary_plan_t* P) {
   if (!P) { set_error("null plan"); return LEANOT_EINVAL; }
   LEANOT_TRY(validate_cost(&P->cost));
-  if (P->n != P->cost.n || P->row0 != 0 || P->row1 != P->n || P->ns < P->n || (P->ns & 1) || P->m < 1 ||
-      P->m > LEANOT_MAX_K || P->splits < 1 ||
-      P->nblk_upd < 1 || P->nblk_upd > 1024) {
-    set_error("inconsistent barycenter plan (single-process plans cover all rows; 1 <= m <= 16)");
+  if (P->n != P->cost.n || P->row0 < 0 || P->row1 > P->n || P->row0 >= P->row1 || P->ns < P->n || (P->ns & 1) ||
+      P->m < 1 || P->m > LEANOT_MAX_K || P->splits < 1 || P->nblk_upd < 1 || P->nblk_upd > 1024) {
+    set_error("inconsistent barycenter plan (rows 0 <= row0 < row1 <= n; 1 <= m <= 16)");
     return LEANOT_EINVAL;
   }
   if (!(P->prm.eta > 0)) { set_error("barycenter solver requires eta > 0"); return LEANOT_EINVAL; }
@@ -158,6 +157,10 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
   cudaStream_t st = S_(stream);
   const int64_t n = P->n, nr = P->row1 - P->row0;
   const int m = P->m;
+  if (nr != n) {
+    set_error("row-sharded barycenter plans sweep through leanot_bary_rows / _rnorm / _cols");
+    return LEANOT_EINVAL;
+  }
   if (use_sep_bary(*P)) {
     // grid cost: separable O(n^1.5) row normalizers, r-maps, separable column sums
     LEANOT_TRY(sep_bary_rows(*P, (flags & LEANOT_SWEEP_EVAL) != 0, st));
@@ -225,8 +228,76 @@ int leanot_bary_eval(const leanot_bary_plan_t* P, void* stream) {
     LEANOT_TRY(launch_rowlse(make_view(P->cost), P->row0, P->row1, P->sd + k * P->ns, 1.0, -1.0 / P->prm.eta,
                              P->L + (int64_t)k * nr, st));
   }
-  bary_dual_reduce_kernel<<<1, 1024, 0, st>>>(P->L, P->w, m, n, P->evalbuf + 127);
+  // LSE over this plan's rows (all rows single-process; a shard's rows otherwise, combined by the caller)
+  bary_dual_reduce_kernel<<<1, 1024, 0, st>>>(P->L, P->w, m, nr, P->evalbuf + 127);
   return check_launch("bary_eval");
+}
+
+// ---- row-sharded sweep (multi-GPU): three phases around the caller's collectives ----
+
+int leanot_bary_rows(const leanot_bary_plan_t* P, int flags, double* gmax, void* stream) {
+  LEANOT_TRY(validate_bary(P));
+  LEANOT_TRY(ensure_init());
+  if (!gmax) { set_error("bary_rows: null gmax"); return LEANOT_EINVAL; }
+  cudaStream_t st = S_(stream);
+  const int64_t n = P->n, nr = P->row1 - P->row0;
+  const int m = P->m;
+  for (int k = 0; k < m; ++k) {
+    RowPassArgs A = bary_rowpass(*P, k);
+    LEANOT_TRY(launch_rowpass(A, 2, (flags & LEANOT_SWEEP_EVAL) != 0, st));
+  }
+  const int64_t tot = (int64_t)m * 2 * nr;
+  const int g = (int)std::min<int64_t>((tot + 255) / 256, 4096);
+  bary_lse_kernel<<<g, 256, 0, st>>>(P->mu, P->S, m, nr, P->L);
+  // g_w,i (sorted k-sum, barycenter.py:90-97) into r[w][row0 + i]; local maxima -> gmax[w]
+  const int nblk = (int)std::min<int64_t>((nr + 255) / 256, 1024);
+  for (int w = 0; w < 2; ++w) {
+    bary_g_kernel<<<nblk, 256, 0, st>>>(P->L + (int64_t)w * m * nr, m, nr, P->w, P->r + (int64_t)w * n + P->row0,
+                                        P->partial);
+    reduce_max_kernel<<<1, 1024, 0, st>>>(P->partial, nblk, gmax + w);
+  }
+  return check_launch("bary_rows");
+}
+
+int leanot_bary_rnorm(const leanot_bary_plan_t* P, const double* gmax, double* esum, void* stream) {
+  LEANOT_TRY(validate_bary(P));
+  LEANOT_TRY(ensure_init());
+  if (!gmax || !esum) { set_error("bary_rnorm: null scalars"); return LEANOT_EINVAL; }
+  cudaStream_t st = S_(stream);
+  const int64_t n = P->n, nr = P->row1 - P->row0;
+  const int nblk = (int)std::min<int64_t>((nr + 255) / 256, 1024);
+  for (int w = 0; w < 2; ++w) {
+    double* rw = P->r + (int64_t)w * n + P->row0;
+    // e_i = exp(g_i - global max), block partial sums, then their fixed-order total
+    bary_e_kernel<<<nblk, 256, 0, st>>>(rw, nr, gmax + w, 1, rw, P->partial);
+    sum_fixed_kernel<<<1, 1024, 0, st>>>(P->partial, nblk, esum + w);
+  }
+  return check_launch("bary_rnorm");
+}
+
+int leanot_bary_cols(const leanot_bary_plan_t* P, const double* esum, void* stream) {
+  LEANOT_TRY(validate_bary(P));
+  LEANOT_TRY(ensure_init());
+  if (!esum) { set_error("bary_cols: null esum"); return LEANOT_EINVAL; }
+  cudaStream_t st = S_(stream);
+  const int64_t n = P->n, nr = P->row1 - P->row0;
+  const int m = P->m;
+  const int nblk = (int)std::min<int64_t>((nr + 255) / 256, 1024);
+  for (int w = 0; w < 2; ++w) bary_norm_kernel<<<nblk, 256, 0, st>>>(P->r + (int64_t)w * n + P->row0, nr, esum + w, 1);
+  const int64_t tot = (int64_t)m * 2 * nr;
+  const int g = (int)std::min<int64_t>((tot + 255) / 256, 4096);
+  bary_coef_kernel<<<g, 256, 0, st>>>(P->S, P->r, m, nr, P->row0, n, P->coef);
+  for (int k = 0; k < m; ++k) {
+    ColPassArgs B;
+    memset(&B, 0, sizeof(B));
+    B.cost = make_view(P->cost); B.i0 = P->row0; B.i1 = P->row1; B.a = P->scal;
+    B.b[0] = P->b + k * P->ns; B.b[1] = P->b_bar + k * P->ns;
+    B.m = P->mu + (int64_t)k * 2 * nr; B.coef = P->coef + (int64_t)k * 2 * nr * 4; B.slab = P->slab;
+    B.splits = P->splits;
+    LEANOT_TRY(launch_colpass(B, 2, st));
+    LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, n, P->col + (int64_t)k * 2 * n, st));
+  }
+  return check_launch("bary_cols");
 }
 
 }  // extern "C"

@@ -484,7 +484,8 @@ static int sep_dxg_eval(const leanot_dxg_plan_t& P, cudaStream_t st) {
 
 // ---- barycenter (leanot_bary.cu) on a grid cost -------------------------------------
 static bool use_sep_bary(const leanot_bary_plan_t& P) {
-  return P.cost.kind == LEANOT_COST_GRID && sep_enabled_env();
+  // single-process plans only: row-sharded (multi-GPU) barycenters take the dense sweeps
+  return P.cost.kind == LEANOT_COST_GRID && P.row0 == 0 && P.row1 == P.n && sep_enabled_env();
 }
 
 // batched scratch of the barycenter plans: 4 (m x n) blocks after the separable layout

@@ -373,6 +373,14 @@ __global__ void bary_norm_kernel(double* r, int64_t n, const double* psum, int n
     r[i] = r[i] / s;
 }
 
+// out = sum of p[0..cnt) in a fixed order (strided per-thread sums, then block_sum)
+__global__ void sum_fixed_kernel(const double* p, int cnt, double* out) {
+  double t = 0.0;
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) t += p[q];
+  t = block_sum(t);
+  if (threadIdx.x == 0) out[0] = t;
+}
+
 // full r-map over all SMs; partial needs 2 * nblk doubles (nblk <= 1024)
 static void launch_rmap(const double* L, int m, int64_t n, const double* w, double* g, double* partial, double* r,
                         cudaStream_t st) {

@@ -55,3 +55,92 @@ def test_engine_shards_combine_to_unsharded_sweep():
     full = cols[2].cpu().numpy()
     got = out.cpu().numpy()
     assert np.max(np.abs(got - full)) <= 1e-13 * np.max(np.abs(full))
+
+
+def _bary_setup(n, m, seed):
+    from paper_2511_11359_b200 import core, dxg
+    rng = np.random.default_rng(seed)
+    f = rng.random((n, 2))
+    marg = [core.Histogram.normalized(rng.random(n)) for _ in range(m)]
+    prm = dxg.params_tuned(1e-2).with_overrides(tau_mu=0.05)
+    return f, marg, prm
+
+
+def _kernel_rows(f, rows):
+    from paper_2511_11359_b200 import core
+    k = core.ColorKernel(f, 2, scale=2.0)
+    if rows is not None:
+        k.row0, k.row1 = rows
+    return k
+
+
+def test_sharded_barycenter_matches_single_process():
+    """Barycenter row sharding: two row shards driven in lockstep on one GPU,
+    with the three exchanges of a multi-GPU iteration done here (max of the r-map maxima,
+    rank-order sums of the exp-sums and of the 2 m n column partials), track the
+    single-process barycenter iteration and evaluation."""
+    import torch
+    from paper_2511_11359_b200 import _lib
+    from paper_2511_11359_b200.barycenter import BaryEngine, _combine_eval_buffers
+    n, m, iters = 3000, 3, 6
+    f, marg, prm = _bary_setup(n, m, 7)
+    w = np.array([0.2, 0.5, 0.3])
+    full = BaryEngine(_kernel_rows(f, None), marg, w, prm)
+    shards = [BaryEngine(_kernel_rows(f, rows), marg, w, prm) for rows in ((0, 1401), (1401, n))]
+    assert all(e.sharded for e in shards) and not full.sharded
+    rng = np.random.default_rng(1)
+    deltas = rng.uniform(-1, 1, (m, n))
+    bs = -np.abs(rng.normal(0, 3, (m, n)))
+    bs -= bs.max(axis=1, keepdims=True)
+    for e in [full] + shards:
+        e.load_state(deltas, bs, 20.0, 0.01, 40)
+
+    def rank_sum(ts):
+        g = torch.cat([t.reshape(-1) for t in ts])
+        out = torch.empty_like(ts[0].reshape(-1))
+        _lib.check(_lib.lib().leanot_sum_partials(g.data_ptr(), len(ts), out.numel(), out.data_ptr(),
+                                                  _lib.stream_handle()), "sum_partials")
+        return out.view(ts[0].shape)
+
+    def sharded_sweep(evaluate=False):
+        for e in shards:
+            e.sweep_rows(evaluate)
+        gm = torch.maximum(shards[0].gmax, shards[1].gmax)
+        for e in shards:
+            e.gmax.copy_(gm)
+            e.sweep_rnorm()
+        es = rank_sum([e.esum for e in shards])
+        for e in shards:
+            e.esum.copy_(es)
+            e.sweep_cols()
+        col = rank_sum([e.col for e in shards])
+        for e in shards:
+            e.col.copy_(col)
+
+    for _ in range(iters):
+        full.sweep()
+        full.update()
+        sharded_sweep()
+        for e in shards:
+            e.update()
+    st_full = full.read_state()
+    for e in shards:
+        st = e.read_state()
+        assert np.max(np.abs(st[0] - st_full[0])) <= 1e-11 * np.max(np.abs(st_full[0]))
+        assert np.max(np.abs(st[1] - st_full[1])) <= 1e-11 * np.max(np.abs(st_full[1]))
+        assert st[2:] == st_full[2:]
+    # evaluation: combined per-shard buffers == single-process buffer
+    full.sweep(evaluate=True)
+    sharded_sweep(evaluate=True)
+    r_full = full.r[:n].cpu().numpy()
+    r_sh = np.concatenate([shards[0].r[:1401].cpu().numpy(), shards[1].r[1401:n].cpu().numpy()])
+    assert np.max(np.abs(r_sh - r_full)) <= 1e-12 * np.max(r_full)
+    full._call("leanot_bary_eval")
+    bufs = []
+    for e in shards:
+        e._call("leanot_bary_eval")
+        bufs.append(e.evalbuf.cpu().numpy())
+    comb = _combine_eval_buffers(bufs, m)
+    ref = full.evalbuf.cpu().numpy()
+    for j in [4 * k for k in range(m)] + [4 * k + 1 for k in range(m)] + [64 + 2 * k for k in range(m)] + [127]:
+        assert abs(comb[j] - ref[j]) <= 1e-11 * max(1.0, abs(ref[j])), j

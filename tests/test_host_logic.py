@@ -90,3 +90,25 @@ def test_product_path_fails_loudly_without_cuda():
     from paper_2511_11359_b200 import core
     with pytest.raises(RuntimeError, match="CUDA"):
         core.GridKernel(3, 3, 2)
+
+
+def test_barycenter_eval_combine_of_row_shards():
+    """Sharded barycenter evaluation (barycenter._combine_eval_buffers): row sums add in rank
+    order, column statistics are taken from rank 0 (identical on all ranks), and the dual's
+    log-sum-exp over rows combines the per-shard LSEs exactly."""
+    import numpy as np
+    from paper_2511_11359_b200.barycenter import _combine_eval_buffers
+    rng = np.random.default_rng(0)
+    m = 3
+    bufs = [rng.normal(size=128) for _ in range(3)]
+    for b in bufs[1:]:
+        for k in range(m):
+            b[64 + 2 * k: 66 + 2 * k] = bufs[0][64 + 2 * k: 66 + 2 * k]
+    out = _combine_eval_buffers(bufs, m)
+    for k in range(m):
+        assert out[4 * k] == (bufs[0][4 * k] + bufs[1][4 * k]) + bufs[2][4 * k]
+        assert out[4 * k + 1] == (bufs[0][4 * k + 1] + bufs[1][4 * k + 1]) + bufs[2][4 * k + 1]
+        assert out[64 + 2 * k] == bufs[0][64 + 2 * k]
+    ls = np.array([b[127] for b in bufs])
+    assert abs(out[127] - np.log(np.exp(ls).sum())) <= 1e-14 * abs(out[127]) + 1e-15
+    assert np.array_equal(_combine_eval_buffers([bufs[0]], m), bufs[0])
