@@ -144,3 +144,53 @@ def test_sharded_barycenter_matches_single_process():
     ref = full.evalbuf.cpu().numpy()
     for j in [4 * k for k in range(m)] + [4 * k + 1 for k in range(m)] + [64 + 2 * k for k in range(m)] + [127]:
         assert abs(comb[j] - ref[j]) <= 1e-11 * max(1.0, abs(ref[j])), j
+
+
+def test_sharded_dxg_iterations_match_single_process():
+    """DXG row sharding: two shards in lockstep on one GPU (the per-iteration exchange of the
+    2n column partials done with the device rank-order sum), 10 iterations and an evaluation,
+    against the unsharded engine."""
+    import torch
+    from paper_2511_11359_b200 import _lib, core, dxg
+    from paper_2511_11359_b200.engine import DxgEngine
+    n, cut = 16000, 7001
+    rng = np.random.default_rng(9)
+    r = rng.random(n); r /= r.sum()
+    c = rng.random(n); c /= c.sum()
+    prm = dxg.params_tuned(1e-3).with_overrides(tau_mu=0.05)
+    engs = [DxgEngine(core.HashKernel(n, seed=2, rows=rows) if rows else core.HashKernel(n, seed=2), r, c, prm)
+            for rows in (None, (0, cut), (cut, n))]
+    for e in engs:
+        e.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
+
+    def rank_sum(ts):
+        g = torch.cat([t.reshape(-1) for t in ts])
+        out = torch.empty_like(ts[0].reshape(-1))
+        _lib.check(_lib.lib().leanot_sum_partials(g.data_ptr(), len(ts), out.numel(), out.data_ptr(),
+                                                  _lib.stream_handle()), "sum_partials")
+        return out
+
+    full, s0, s1 = engs
+    for it in range(10):
+        ev = it == 9
+        for e in engs:
+            e.sweep(evaluate=ev)
+        col = rank_sum([s0.col, s1.col])
+        s0.col.copy_(col); s1.col.copy_(col)
+        if ev:
+            break
+        for e in engs:
+            e.update()
+    assert np.max(np.abs(s0.col.cpu().numpy() - full.col.cpu().numpy())) <= 1e-13
+    with torch.cuda.device(0):
+        for e in engs:
+            _lib.check(_lib.lib().leanot_dxg_eval(__import__("ctypes").byref(e.plan), _lib.stream_handle()), "eval")
+    b_full = full.evalbuf[:5].cpu().numpy()
+    rows = rank_sum([s0.evalbuf[:3], s1.evalbuf[:3]]).cpu().numpy()
+    assert np.max(np.abs(rows - b_full[:3])) <= 1e-12 * np.max(np.abs(b_full[:3]))
+    assert np.max(np.abs(s0.evalbuf[3:5].cpu().numpy() - b_full[3:5])) <= 1e-12 * np.max(np.abs(b_full[3:5]))
+    d_full, b_f, a_f, s_f, t_f = full.read_state()
+    d_0, b_0, a_0, s_0, t_0 = s0.read_state()
+    assert np.max(np.abs(d_0 - d_full)) <= 1e-11 * max(1e-300, np.max(np.abs(d_full)))
+    assert np.max(np.abs(b_0 - b_f)) <= 1e-11 * max(1.0, np.max(np.abs(b_f)))
+    assert (a_0, s_0, t_0) == (a_f, s_f, t_f)
