@@ -67,7 +67,7 @@ __device__ __forceinline__ double block_sum_bcast(double v, double* red) {
 // max of cnt block maxima, loaded in parallel by the block (max is order-independent)
 __device__ __forceinline__ double max_over(const double* p, int cnt, double* red) {
   double t = -INFINITY;
-  for (int q = threadIdx.x; q < cnt; q += PS_THREADS) t = fmax(t, p[q]);
+  for (int q = threadIdx.x; q < cnt; q += PS_THREADS) t = fmax(t, __ldcg(p + q));  // written by other CTAs
   return block_max_bcast(t, red);
 }
 
@@ -306,6 +306,370 @@ __global__ void __launch_bounds__(PS_THREADS) dxg_persist_kernel(const PersistAr
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Row-owner persistent iterations for n <= 1024 (BASELINE config 1): the single-read form.
+// CTA c owns rows [c R, c R + R) (R = ceil(n / G) <= 8) and keeps their exps in registers
+// (256 threads x 4 columns x R rows x 2 weight sets), so pass B is an FMA over the stored
+// exps instead of a second exp and needs no grid barrier after pass A (the row sums are
+// CTA-local).  Per iteration two grid barriers instead of four:
+//   A+B (own rows) -> slab[c][k][j] | sync | column owners: fixed-order sum of the G partials,
+//   dual_md_step / balance / b' (dxg.py:223-258), block max | sync | every CTA: b, sd, b_bar'
+//   for all n columns (redundant, bitwise identical), max b_bar' locally, b_bar in shared
+//   memory; owners write the state back.  Same per-element arithmetic (table exp, shifts from
+//   the previous iteration, exact-max recompute of out-of-range rows) and fixed reduction
+//   orders; the column sums are sum_i g_i e_ij with the product formed after the exp
+//   (the regular pass B folds g into the polynomial: same value to a few ulps).
+constexpr int PO_THREADS = 512;            // 16 warps: latency hiding for the exp chains
+constexpr int PO_WARPS = PO_THREADS / 32;
+constexpr int PO_J = 2;                    // columns per thread (n <= 1024)
+constexpr int PO_R = 8;                    // max rows per CTA
+constexpr int64_t PO_MAX_N = PO_THREADS * PO_J;
+constexpr int PO_PARTS = 6;                // partials per lane in the column sums (G <= 192)
+
+__device__ __forceinline__ double po_block_max(double v, double* red) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = red[0];
+#pragma unroll
+  for (int w = 1; w < PO_WARPS; ++w) t = fmax(t, red[w]);
+  __syncthreads();
+  return t;
+}
+__device__ __forceinline__ double po_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = red[0];
+#pragma unroll
+  for (int w = 1; w < PO_WARPS; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+__device__ __forceinline__ double po_max_over(const double* p, int cnt, double* red) {
+  double t = -INFINITY;
+  for (int q = threadIdx.x; q < cnt; q += PO_THREADS) t = fmax(t, __ldcg(p + q));  // written by other CTAs
+  return po_block_max(t, red);
+}
+
+#ifdef LEANOT_DBG_TIMING
+#define PO_TS(slot)                                                                     \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && it == 5) {                               \
+      uint64_t t_;                                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      reinterpret_cast<uint64_t*>(const_cast<double*>(P.U.partial))[slot] = t_;         \
+    }                                                                                   \
+  } while (0)
+#else
+#define PO_TS(slot) do {} while (0)
+#endif
+
+template <class COST>
+__global__ void __launch_bounds__(PO_THREADS, 1) dxg_rowowner_kernel(const PersistArgs P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) char smem[];
+  const UpdArgs& U = P.U;
+  const int64_t n = U.n;
+  double* sb = reinterpret_cast<double*>(smem + TAB_BYTES);  // b, all n
+  double* sbb = sb + PO_MAX_N;                                // b_bar, all n
+  double* sC = sbb + PO_MAX_N;                                // own rows of C [PO_R][n] (constant)
+  __shared__ double red[PO_WARPS];
+  __shared__ double pred[PO_WARPS][2 * PO_R];
+  __shared__ double sS[2 * PO_R], sg[2 * PO_R];
+  __shared__ int64_t smk[2 * PO_R];
+  __shared__ double scol[32];
+  load_table(reinterpret_cast<double*>(smem));
+  const int G = gridDim.x, c = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t j = threadIdx.x; j < n; j += PO_THREADS) { sb[j] = U.b[j]; sbb[j] = U.b_bar[j]; }
+  double sc[4];  // a, a_bar, s, t (every CTA advances its own copy; CTA 0 publishes)
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sc[q] = U.scal[q];
+  __syncthreads();
+  const uint32_t tb = lane_tab_addr(smem);
+  const COST cost(P.cost);
+  const int rpc = (int)((n + G - 1) / G);
+  const int64_t i0 = (int64_t)c * rpc;
+  const int nrow = (int)(i0 >= n ? 0 : (n - i0 < rpc ? n - i0 : rpc));
+  const int grows = (int)((n + rpc - 1) / rpc);  // CTAs that own rows
+  const int cpc = rpc;                           // columns owned per CTA (same split)
+  const int64_t j0c = (int64_t)c * cpc;
+  const int ncol = (int)(j0c >= n ? 0 : (n - j0c < cpc ? n - j0c : cpc));
+  // the own rows' costs stay in shared memory for the whole launch (pass A reads them with
+  // LDS latency instead of one dependent global load per element)
+  for (int q = 0; q < nrow; ++q) {
+    const typename COST::Row rq = cost.row(i0 + q);
+    for (int64_t j = threadIdx.x; j < n; j += PO_THREADS) sC[q * n + j] = cost.eval1(rq, j);
+  }
+  double rw[PO_R];
+#pragma unroll
+  for (int q = 0; q < PO_R; ++q) rw[q] = q < nrow ? P.r[i0 + q] : 0.0;
+  // owner threads keep their column's marginal constants and dual in registers (only the
+  // owner writes delta_j; everybody else reads it after the second barrier)
+  const bool owner = threadIdx.x < ncol;
+  const int64_t jo = owner ? j0c + threadIdx.x : 0;
+  const double c_o = owner ? U.c[jo] : 0.0, ct_o = owner ? U.ct[jo] : 1.0;
+  double d_o = owner ? U.delta[jo] : 0.0;
+  __syncthreads();
+
+  for (int it = 0; it < P.iters; ++it) {
+    const double na[2] = {-sc[0], -sc[1]};
+    PO_TS(0);
+    // ---- pass A on the own rows; exps kept in registers ----
+    double e[PO_R][PO_J][2], s[PO_R][2];
+    uint32_t mlo[PO_R];
+    int64_t msh[PO_R];
+#pragma unroll
+    for (int q = 0; q < PO_R; ++q) {
+      msh[q] = q < nrow ? P.shift[i0 + q] : 0;
+      mlo[q] = (uint32_t)msh[q];
+      s[q][0] = s[q][1] = 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PO_J; ++u) {
+      const int64_t j = threadIdx.x + (int64_t)PO_THREADS * u;
+      const bool valid = j < n;
+      const int64_t jj = valid ? j : 0;
+      const double nb0 = -sb[jj], nb1 = -sbb[jj];
+#pragma unroll
+      for (int q = 0; q < PO_R; ++q) {
+        // rows q >= nrow / columns j >= n compute on a valid (unused) operand and are masked
+        const double cq = sC[(q < nrow ? q : 0) * n + jj];
+        const bool on = q < nrow && valid;
+        const double e0 = texp(tb, fma(na[0], cq, nb0), mlo[q]);
+        const double e1 = texp(tb, fma(na[1], cq, nb1), mlo[q]);
+        e[q][u][0] = on ? e0 : 0.0;
+        e[q][u][1] = on ? e1 : 0.0;
+        s[q][0] += e[q][u][0];
+        s[q][1] += e[q][u][1];
+      }
+    }
+    // block sums of the 2 R row sums: per-warp transpose-reduce (value (lane >> 1) & 15 on
+    // even lanes), then the warps in order
+    {
+      double v8[8], v4[4], v2[2];
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double lo = s[i >> 1][i & 1], hi = s[(i + 8) >> 1][(i + 8) & 1];
+        v8[i] = (b4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        v4[i] = (b3 ? v8[i + 4] : v8[i]) + __shfl_xor_sync(0xffffffffu, b3 ? v8[i] : v8[i + 4], 8);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        v2[i] = (b2 ? v4[i + 2] : v4[i]) + __shfl_xor_sync(0xffffffffu, b2 ? v4[i] : v4[i + 2], 4);
+      double x = (b1 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? v2[0] : v2[1], 2);
+      x += __shfl_xor_sync(0xffffffffu, x, 1);
+      if ((lane & 1) == 0) pred[warp][(lane >> 1) & 15] = x;
+    }
+    PO_TS(1);
+    __syncthreads();
+    if (threadIdx.x < 2 * PO_R) {
+      double t = pred[0][threadIdx.x];
+#pragma unroll
+      for (int w = 1; w < PO_WARPS; ++w) t += pred[w][threadIdx.x];
+      sS[threadIdx.x] = t;
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < PO_R; ++q) smk[2 * q] = smk[2 * q + 1] = msh[q];
+    }
+    __syncthreads();
+    // out-of-range sums: exact max shift for that row and weight set, exps recomputed
+#pragma unroll
+    for (int q = 0; q < PO_R; ++q)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (q >= nrow || sum_ok(sS[2 * q + k])) continue;  // block-uniform
+        const double* bk = k == 0 ? sb : sbb;
+        const double* cr = sC + q * n;
+        double mx = -INFINITY;
+        for (int64_t j = threadIdx.x; j < n; j += PO_THREADS) mx = fmax(mx, fma(na[k], cr[j], -bk[j]));
+        mx = po_block_max(mx, red);
+        const int64_t m = llrint(mx * (1.0 / LSTEP));
+        double t = 0.0;
+#pragma unroll
+        for (int u = 0; u < PO_J; ++u) {
+          const int64_t j = threadIdx.x + (int64_t)PO_THREADS * u;
+          e[q][u][k] = j < n ? texp(tb, fma(na[k], cr[j], -bk[j]), (uint32_t)m) : 0.0;
+          t += e[q][u][k];
+        }
+        t = po_block_sum(t, red);
+        if (threadIdx.x == 0) {
+          sS[2 * q + k] = t;
+          smk[2 * q + k] = m;
+        }
+        __syncthreads();
+      }
+    // finalize the own rows (dxg outputs, next-iteration shift from the midpoint set)
+    if (threadIdx.x < 2 * PO_R) {
+      const int q = threadIdx.x >> 1, k = threadIdx.x & 1;
+      if (q < nrow) {
+        const int64_t i = i0 + q;
+        const double Sk = sS[threadIdx.x];
+        P.S[k * n + i] = Sk;
+        P.m[k * n + i] = smk[threadIdx.x];
+        double rq = rw[0];
+#pragma unroll
+        for (int qq = 1; qq < PO_R; ++qq) rq = q == qq ? rw[qq] : rq;
+        sg[threadIdx.x] = rq / Sk;
+        if (k == 1) P.shift[i] = smk[threadIdx.x] + llrint(log(Sk) * (1.0 / LSTEP));
+      } else {
+        sg[threadIdx.x] = 0.0;
+      }
+    }
+    __syncthreads();
+    PO_TS(2);
+    // ---- pass B on the own rows: column partials from the stored exps ----
+#pragma unroll
+    for (int u = 0; u < PO_J; ++u) {
+      const int64_t j = threadIdx.x + (int64_t)PO_THREADS * u;
+      if (j < n && c < grows) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < PO_R; ++q) {
+          a0 = fma(sg[2 * q], e[q][u][0], a0);
+          a1 = fma(sg[2 * q + 1], e[q][u][1], a1);
+        }
+        P.slab[((int64_t)c * 2) * n + j] = a0;
+        P.slab[((int64_t)c * 2 + 1) * n + j] = a1;
+      }
+    }
+    PO_TS(3);
+    grid.sync();
+    PO_TS(4);
+    // ---- owned columns: fixed-order sum of the partials (16 lanes per value), updates ----
+    {
+      const int v = threadIdx.x >> 5, part = threadIdx.x & 31;  // value v = 2 * column + set
+      double t = 0.0;
+      if (v < 2 * ncol) {
+        // all of this lane's partials in flight at once, then added in order
+        const int64_t j = j0c + (v >> 1);
+        double pv[PO_PARTS];
+#pragma unroll
+        for (int u = 0; u < PO_PARTS; ++u) {
+          const int p = part + 32 * u;
+          pv[u] = p < grows ? __ldcg(P.slab + ((int64_t)p * 2 + (v & 1)) * n + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PO_PARTS; ++u) t += pv[u];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (part == 0 && v < 16) scol[v] = t;
+    }
+    __syncthreads();
+    double mx = -INFINITY;
+    if (owner) {
+      const int64_t j = jo;
+      const double cn = scol[2 * threadIdx.x], cb = scol[2 * threadIdx.x + 1];
+      const_cast<double*>(U.col)[j] = cn;
+      const_cast<double*>(U.col)[n + j] = cb;
+      const double dbar = md_step(U.A, U.B, d_o, cn, c_o, ct_o);
+      double dn = md_step(U.A, U.B, d_o, cb, c_o, ct_o);
+      dn = fmin(fmax(dn, -U.beta), U.beta);
+      const double bp = __dadd_rn(__dmul_rn(U.decay, sb[j]), __dmul_rn(U.G, tanh(__dmul_rn(0.5, dbar))));
+      d_o = dn;
+      U.delta[j] = dn;
+      U.bprime[j] = bp;
+      mx = bp;
+    }
+    mx = po_block_max(mx, red);
+    if (threadIdx.x == 0) P.gmax[c] = mx;
+    PO_TS(5);
+    grid.sync();
+    PO_TS(6);
+    // ---- every CTA: b = b' - max b', sd, b_bar' for all columns; b_bar = b_bar' - max ----
+    {
+      // loads of b' and delta first (independent of the max), so both latencies overlap
+      double bpv[PO_J], dv[PO_J];
+#pragma unroll
+      for (int u = 0; u < PO_J; ++u) {
+        const int64_t j = threadIdx.x + (int64_t)PO_THREADS * u;
+        bpv[u] = j < n ? __ldcg(U.bprime + j) : 0.0;
+        dv[u] = j < n ? tanh(__dmul_rn(0.5, __ldcg(U.delta + j))) : 0.0;
+      }
+      const double M = po_max_over(P.gmax, G, red);
+      double mb = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < PO_J; ++u) {
+        const int64_t j = threadIdx.x + (int64_t)PO_THREADS * u;
+        if (j < n) {
+          const double bn = __dsub_rn(bpv[u], M);
+          const double d = dv[u];
+          const double bb = __dadd_rn(__dmul_rn(U.decay, bn), __dmul_rn(U.G, d));
+          sb[j] = bn;
+          sbb[j] = bb;
+          mb = fmax(mb, bb);
+          if (j >= j0c && j < j0c + ncol) {
+            U.b[j] = bn;
+            U.sd[j] = __dmul_rn(U.twosup, d);
+          }
+        }
+      }
+      mb = po_block_max(mb, red);
+#pragma unroll
+      for (int u = 0; u < PO_J; ++u) {
+        const int64_t j = threadIdx.x + (int64_t)PO_THREADS * u;
+        if (j < n) {
+          const double bb = __dsub_rn(sbb[j], mb);
+          sbb[j] = bb;
+          if (j >= j0c && j < j0c + ncol) U.b_bar[j] = bb;
+        }
+      }
+      const double a = __dadd_rn(__dmul_rn(U.decay, sc[0]), U.tau_p);
+      sc[0] = a;
+      sc[1] = __dadd_rn(__dmul_rn(U.decay, a), U.tau_p);
+      sc[2] = __dadd_rn(__dmul_rn(U.decay, sc[2]), U.tau_p_eta);
+      sc[3] = sc[3] + 1.0;
+      __syncthreads();
+    }
+    PO_TS(7);
+  }
+  if (c == 0 && threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) U.scal[q] = sc[q];
+  }
+}
+
+static inline int64_t a_n(const PersistArgs& P) { return P.U.n; }
+
+struct RowOwnerFn {
+  const PersistArgs& P;
+  int64_t slab_doubles;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    auto kern = dxg_rowowner_kernel<COST>;
+    const size_t smem = TAB_BYTES + 2 * PO_MAX_N * 8 + (size_t)PO_R * a_n(P) * 8;
+    static bool attr = false;  // per instantiation
+    if (!attr) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return LEANOT_EINVAL;
+      attr = true;
+    }
+    PersistArgs a = P;
+    const int64_t n = a.U.n;
+    const int G = num_sms();
+    if ((n + G - 1) / G > PO_R || n > PO_MAX_N || G > 32 * PO_PARTS) return LEANOT_EINVAL;
+    if ((int64_t)G * 2 * n + G > slab_doubles) return LEANOT_EINVAL;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PO_THREADS, smem) != cudaSuccess || occ < 1)
+      return LEANOT_EINVAL;
+    a.gmax = a.slab + (int64_t)G * 2 * n;
+    void* args[] = {&a};
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, G, PO_THREADS, args, smem, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return LEANOT_EINVAL;
+    }
+    return LEANOT_OK;
+  }
+};
+
 struct PersistFn {
   const PersistArgs& P;
   int blocks_per_sm, max_splits;
@@ -348,6 +712,16 @@ struct PersistFn {
   }
 };
 
+// LEANOT_ROWOWNER=0 keeps the four-barrier persistent kernel for n <= 1024 (A/B comparisons)
+static bool rowowner_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LEANOT_ROWOWNER");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool persist_env() {
   static int v = -1;
   if (v < 0) {
@@ -377,6 +751,10 @@ static int try_persist_iterate(const leanot_dxg_plan_t& P, int iters, cudaStream
   A.splits = 0;
   A.ntile = (int)((n + 31) / 32);
   A.iters = iters;
+  if (n <= PO_MAX_N && rowowner_env()) {
+    RowOwnerFn g{A, (int64_t)P.splits * 2 * n, st};
+    if (LEANOT_DISPATCH_COST(A.cost, g) == LEANOT_OK) return LEANOT_OK;
+  }
   PersistFn f{A, 2, P.splits, (size_t)(TAB_BYTES + ((n + 1) & ~int64_t(1)) * 8), st};
   return LEANOT_DISPATCH_COST(A.cost, f);
 }

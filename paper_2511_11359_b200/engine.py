@@ -107,6 +107,8 @@ class DxgEngine:
         self.S = torch.zeros(2 * nr, **f64)
         self.coef = torch.zeros(8 * nr, **f64)
         self.rowstat = torch.zeros(3 * nr, **f64)
+        if n <= 1024:   # row-owner persistent kernel (csrc/leanot_persist.cu): one partial per CTA
+            splits = max(int(splits), self._sms() + 1)
         slab = splits * 2 * n
         if kernel.cost_struct().kind == _lib.COST_GRID:   # separable path scratch (leanot_sep.cu)
             slab = max(slab, int(L.leanot_grid_sep_ws_doubles(kernel.cost_struct())))
