@@ -1,0 +1,208 @@
+"""SPEC.md acceptance criteria on the CUDA path (needs a B200).
+
+The reference ships no tests; its SPEC's acceptance criteria are the intended ones
+(SURVEY.md §4).  Criterion 2 (rounding guarantee) is in test_gpu_dense.py; 5 and 6 are
+properties of the algorithm's host-side formulas (test_host_logic.py).  Oracles: the dense
+PDXG restatement (oracle/leanot_oracle.py:pdxg_step, pinned to the reference by
+tests/test_oracle_golden.py) and the reference's exact LP values (tests/golden/spec_acceptance.npz,
+oracle/gen_golden_spec.py).
+"""
+
+import numpy as np
+import pytest
+
+import leanot_oracle as O
+from helpers import load
+
+pytestmark = pytest.mark.gpu
+
+
+def _mods():
+    from paper_2511_11359_b200 import barycenter, core, dxg, sinkhorn
+    return core, dxg, barycenter, sinkhorn
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_1_pdxg_dxg_iterate_equivalence(n):
+    """Criterion 1: the implicit DXG iterate D_r p equals the dense PDXG iterate (loose
+    parameters, 500 iterations, 20 seeds): max l_inf deviation <= 1e-9."""
+    core, dxg, _, _ = _mods()
+    worst = 0.0
+    for seed in range(20):
+        rng = np.random.default_rng(1000 + seed)
+        C = rng.random((n, n))
+        r = core.Histogram.normalized(rng.random(n) + 0.1)
+        c = core.Histogram.normalized(rng.random(n) + 0.1)
+        k = core.ExplicitKernel(C)
+        prm = dxg.params_loose(n, 1e-2, float(c.weights.min()), k.sup_norm)
+        oprm = O.Params(prm.eta, prm.eta_mu, prm.tau_p, prm.tau_mu, prm.beta, prm.alpha)
+        Cn = C / C.max()
+        st = dxg.DxgState.initial(n)
+        delta, log_p = np.zeros(n), np.full((n, n), -np.log(n))
+        for it in range(1, 501):
+            st = dxg.dxg_step(st, k, r, c, prm)
+            delta, log_p = O.pdxg_step(delta, log_p, Cn, r.weights, c.weights, oprm, 1.0)
+            if it % 50 == 0:
+                plan = dxg.materialize_plan(st.weights, k, r)
+                ref = r.weights[:, None] * np.exp(log_p)
+                worst = max(worst, float(np.max(np.abs(plan - ref))))
+                assert np.max(np.abs(st.mu.delta - delta)) <= 1e-9
+    assert worst <= 1e-9, worst
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_3_penalized_eot_equals_eot(n):
+    """Criterion 3: with eta = 0.5 ||C||_inf / (-log min c~) the converged DXG plan is the
+    EOT plan (Sinkhorn at the same eta): l1 <= 1e-5; the recovered potentials match the
+    mean-centered Sinkhorn potentials: l_inf <= 1e-5."""
+    core, dxg, _, sk = _mods()
+    rng = np.random.default_rng(300 + n)
+    k = core.ExplicitKernel(rng.random((n, n)))
+    r = core.Histogram.normalized(rng.random(n) + 0.1)
+    c = core.Histogram.normalized(rng.random(n) + 0.1)
+    base = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    eta = 0.5 * k.sup_norm / (-np.log(float((c.weights + base.alpha / n).min())))
+    prm = dxg.params_tuned(eta).with_overrides(tau_mu=0.05)
+    sol = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-9, max_iter=200_000), dense_cap=0)
+    plan = dxg.materialize_plan(sol.state.weights, k, r)
+    pot = sk.sinkhorn_solve(k, r, c, eta, tol=1e-13)
+    splan = sk.sinkhorn_plan_dense(pot, k)
+    assert float(np.abs(plan - splan).sum()) <= 1e-5
+    rec = dxg.recover_eot_potentials(sol.state, sol.state.mu, k, r, eta)
+    phi_s = pot.phi - pot.phi.mean()
+    psi_s = pot.psi - pot.psi.mean()
+    assert np.max(np.abs(rec.phi - phi_s)) <= 1e-5 * max(1.0, np.max(np.abs(phi_s)))
+    assert np.max(np.abs(rec.psi - psi_s)) <= 1e-5 * max(1.0, np.max(np.abs(psi_s)))
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_4_rounded_cost_vs_exact_lp(p):
+    """Criterion 4: 8x8 grid, eta = 0, target 1e-4: the rounded DXG plan's cost is within 1e-4
+    of the exact LP optimum (reference oracle.exact_ot) within 1e5 iterations.  tau_mu = 0.05
+    (the tuned tau_mu = 1 never reaches the target)."""
+    core, dxg, _, _ = _mods()
+    d = load("spec_acceptance")
+    k = core.GridKernel(8, 8, p)
+    r, c = core.Histogram(d[f"lp{p}_r"]), core.Histogram(d[f"lp{p}_c"])
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    sol = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-4, max_iter=100_000), dense_cap=64)
+    assert sol.converged and sol.iterations <= 100_000
+    val = float(d[f"lp{p}_value"])
+    assert sol.rounded_cost is not None
+    assert sol.rounded_cost <= val + 1e-4
+    assert sol.rounded_cost >= val - 1e-12            # a feasible plan cannot beat the LP optimum
+
+
+@pytest.mark.parametrize("eta", [0.0, 1e-3])
+def test_7_weak_duality(eta):
+    """Criterion 7: dual_penalized_value <= primal_penalized_value for random states, n <= 16."""
+    core, dxg, _, _ = _mods()
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        n = int(rng.integers(2, 17))
+        k = core.ExplicitKernel(rng.random((n, n)))
+        r = core.Histogram.normalized(rng.random(n) + 0.05)
+        c = core.Histogram.normalized(rng.random(n) + 0.05)
+        w = dxg.TransportLogWeights(float(rng.uniform(0, 50)), -np.abs(rng.normal(0, 5, n)), 0.0, 0)
+        mu = dxg.LogOddsField(rng.uniform(-1.1, 1.1, n))
+        assert dxg.dual_penalized_value(mu, k, r, c, eta) <= dxg.primal_penalized_value(w, k, r, c, eta) + 1e-13
+
+
+def _blobs(side, m, rng):
+    yy, xx = np.mgrid[0:side, 0:side] / (side - 1.0)
+    out = []
+    for _ in range(m):
+        cx, cy, s = rng.uniform(0.25, 0.75), rng.uniform(0.25, 0.75), rng.uniform(0.08, 0.15)
+        h = np.exp(-((xx - cx) ** 2 + (yy - cy) ** 2) / (2 * s * s)).ravel() + 1e-6
+        out.append(h / h.sum())
+    return out
+
+
+def test_8_barycenter_consistency_with_ibp():
+    """Criterion 8: m = 3 shapes on a 16x16 grid, eta = 1e-3: the DXG-B barycenter is within
+    1e-2 (l1) of the IBP barycenter at the same eta."""
+    core, dxg, bary, sk = _mods()
+    rng = np.random.default_rng(8)
+    k = core.GridKernel(16, 16, 2)
+    margs = [core.Histogram(h) for h in _blobs(16, 3, rng)]
+    w = np.ones(3) / 3
+    prm = dxg.params_tuned(1e-3).with_overrides(tau_mu=0.05)
+    sol = bary.dxgb_solve(k, margs, w, prm, dxg.Termination(eps=1e-3, max_iter=200_000))
+    ibp = sk.ibp_barycenter(k, margs, w, 1e-3, tol=1e-10, max_iter=100_000)
+    assert float(np.abs(sol.barycenter.weights - ibp.barycenter.weights).sum()) <= 1e-2
+
+
+@pytest.mark.parametrize("tpe", [0.0, 1e-4, 0.1])
+def test_9_s_t_closed_form(tpe):
+    """Criterion 9: the device recurrence s' = (1 - tau_p eta) s + tau_p eta equals
+    1 - (1 - tau_p eta)^t over 1e4 iterations (2e-14: the reference itself reaches 1.6e-14
+    at tau_p eta = 1e-4)."""
+    core, dxg, _, _ = _mods()
+    from paper_2511_11359_b200.engine import DxgEngine
+    n = 16
+    rng = np.random.default_rng(9)
+    k = core.ExplicitKernel(rng.random((n, n)))
+    r = core.Histogram.normalized(rng.random(n) + 0.1).weights
+    c = core.Histogram.normalized(rng.random(n) + 0.1).weights
+    tau_p = 0.5
+    prm = dxg.DxgParams(eta=tpe / tau_p, eta_mu=0.0, tau_p=tau_p, tau_mu=0.05, beta=1.1, alpha=0.01)
+    eng = DxgEngine(k, r, c, prm)
+    eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
+    for chunk in range(10):
+        eng.iterate(1000)
+        s = eng.scalars()[2]
+        t = 1000 * (chunk + 1)
+        closed = 1.0 - (1.0 - tpe) ** t
+        assert abs(s - closed) <= 2e-14, (t, s, closed)
+
+
+def test_10_linear_memory():
+    """Criterion 10: device memory of a DXG solve (grid kernel) grows linearly: n = 4096 vs
+    n = 1024 at most 5x (an n^2 buffer would be 16x)."""
+    import torch
+    core, dxg, _, _ = _mods()
+    peaks = []
+    for side in (32, 64):
+        n = side * side
+        rng = np.random.default_rng(side)
+        k = core.GridKernel(side, side, 1)
+        r = core.Histogram.normalized(rng.random(n) + 0.1)
+        c = core.Histogram.normalized(rng.random(n) + 0.1)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        dxg.solve(k, r, c, dxg.params_tuned(0.0).with_overrides(tau_mu=0.05),
+                  dxg.Termination(eps=1e-10, max_iter=60), dense_cap=0)
+        torch.cuda.synchronize()
+        peaks.append(torch.cuda.max_memory_allocated() - base)
+    assert peaks[1] <= 5 * peaks[0], peaks
+
+
+def test_11_determinism_byte_identical_trajectories():
+    """Criterion 11: identical inputs give bit-identical trajectories (every logged scalar)
+    and final states, for DXG (stored, points, grid costs), DXG-B and Sinkhorn."""
+    core, dxg, bary, sk = _mods()
+    rng = np.random.default_rng(11)
+    n = 300
+    r = core.Histogram.normalized(rng.random(n) + 0.1)
+    c = core.Histogram.normalized(rng.random(n) + 0.1)
+    C = rng.random((n, n))
+    f = rng.random((n, 3))
+    prm = dxg.params_tuned(1e-3).with_overrides(tau_mu=0.05)
+
+    def traj(sol):
+        return [(p.iter, p.primal, p.dual, p.gap, p.col_infeas_l1, p.s) for p in sol.trajectory]
+
+    for make in (lambda: core.ExplicitKernel(C), lambda: core.ColorKernel(f, 2), lambda: core.GridKernel(15, 20, 1)):
+        runs = [dxg.solve(make(), r, c, prm, dxg.Termination(eps=1e-12, max_iter=400), dense_cap=0) for _ in range(2)]
+        assert traj(runs[0]) == traj(runs[1])
+        assert np.array_equal(runs[0].state.mu.delta, runs[1].state.mu.delta)
+        assert np.array_equal(runs[0].state.weights.b, runs[1].state.weights.b)
+    k = core.GridKernel(12, 12, 2)
+    margs = [core.Histogram(h) for h in _blobs(12, 3, rng)]
+    b = [bary.dxgb_solve(k, margs, np.ones(3) / 3, prm, dxg.Termination(eps=1e-12, max_iter=200)) for _ in range(2)]
+    assert traj(b[0]) == traj(b[1]) and np.array_equal(b[0].barycenter.weights, b[1].barycenter.weights)
+    ke = core.ExplicitKernel(C)
+    s = [sk.sinkhorn_solve(ke, r, c, 1e-2, tol=1e-11) for _ in range(2)]
+    assert np.array_equal(s[0].phi, s[1].phi) and np.array_equal(s[0].psi, s[1].psi)

@@ -153,3 +153,20 @@ def test_ibp_oracle_matches_reference():
         assert conv == bool(info[0]) and sweeps == int(info[1])
         assert rel_err(bary, d[f"{tag}_bary"]) <= 1e-12
         assert rel_err(phis, d[f"{tag}_phis"]) <= 1e-12 and rel_err(psis, d[f"{tag}_psis"]) <= 1e-12
+
+
+def test_oracle_pdxg_matches_reference_dense_iterate():
+    """SPEC acceptance 1 needs the dense PDXG oracle (dxg.py:494-521): the oracle's restatement
+    reproduces the reference's 500-iteration iterate (tests/golden/spec_acceptance.npz)."""
+    d = load("spec_acceptance")
+    for n in (4, 8, 16):
+        p = d[f"pdxg{n}_params"]
+        prm = O.Params(*[float(v) for v in p])
+        C, r, c = d[f"pdxg{n}_C"], d[f"pdxg{n}_r"], d[f"pdxg{n}_c"]
+        sup = 1.0
+        Cn = C / C.max()
+        delta, log_p = np.zeros(n), np.full((n, n), -np.log(n))
+        for _ in range(500):
+            delta, log_p = O.pdxg_step(delta, log_p, Cn, r, c, prm, sup)
+        assert np.max(np.abs(log_p - d[f"pdxg{n}_log_p"])) <= 1e-11
+        assert np.max(np.abs(delta - d[f"pdxg{n}_delta"])) <= 1e-11
