@@ -1,8 +1,8 @@
 """SPEC.md acceptance criteria on the CUDA path (needs a B200).
 
 The reference ships no tests; its SPEC's acceptance criteria are the intended ones
-(SURVEY.md §4).  Criterion 2 (rounding guarantee) is in test_gpu_dense.py; 5 and 6 are
-properties of the algorithm's host-side formulas (test_host_logic.py).  Oracles: the dense
+(SURVEY.md §4).  Criterion 2 (rounding guarantee) is in test_gpu_dense.py; 6 (the clamp is
+the KL projection) is a property of the host-side formula (test_host_logic.py).  Oracles: the dense
 PDXG restatement (oracle/leanot_oracle.py:pdxg_step, pinned to the reference by
 tests/test_oracle_golden.py) and the reference's exact LP values (tests/golden/spec_acceptance.npz,
 oracle/gen_golden_spec.py).
@@ -206,3 +206,36 @@ def test_11_determinism_byte_identical_trajectories():
     ke = core.ExplicitKernel(C)
     s = [sk.sinkhorn_solve(ke, r, c, 1e-2, tol=1e-11) for _ in range(2)]
     assert np.array_equal(s[0].phi, s[1].phi) and np.array_equal(s[0].psi, s[1].psi)
+
+
+def _wkl(plan_star, plan, delta_star, delta, ct, tau_p, tau_mu):
+    """Weighted KL D^w(zeta* || zeta) for m = 1: plans D_r p and the
+    column pairs D_c~ (mu+, mu-) with mu+ = logistic(delta)."""
+    kp = float(np.sum(np.where(plan_star > 0, plan_star * (np.log(plan_star) - np.log(plan)), 0.0)))
+    sp = 1.0 / (1.0 + np.exp(-delta_star))
+    s = 1.0 / (1.0 + np.exp(-delta))
+    km = float(np.sum(ct * (sp * (np.log(sp) - np.log(s)) + (1 - sp) * (np.log1p(-sp) - np.log1p(-s)))))
+    return kp / (2 * tau_p) + km / (2 * tau_mu)
+
+
+def test_5_weighted_kl_contraction():
+    """Criterion 5: n = 16, loose parameters: the weighted KL divergence to a 1e5-iteration
+    reference iterate is nonincreasing (1e-12 slack) over the first 1000 iterations."""
+    core, dxg, _, _ = _mods()
+    n = 16
+    rng = np.random.default_rng(5)
+    k = core.ExplicitKernel(rng.random((n, n)))
+    r = core.Histogram.normalized(rng.random(n) + 0.1)
+    c = core.Histogram.normalized(rng.random(n) + 0.1)
+    prm = dxg.params_loose(n, 1e-2, float(c.weights.min()), k.sup_norm)
+    ct = c.weights + prm.alpha / n
+    star = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-300, max_iter=100_000), dense_cap=0).state
+    plan_star = dxg.materialize_plan(star.weights, k, r)
+    st = dxg.DxgState.initial(n)
+    prev = np.inf
+    for it in range(1000):
+        d = _wkl(plan_star, dxg.materialize_plan(st.weights, k, r), star.mu.delta, st.mu.delta, ct,
+                 prm.tau_p, prm.tau_mu)
+        assert d <= prev + 1e-12, (it, d, prev)
+        prev = d
+        st = dxg.dxg_step(st, k, r, c, prm)

@@ -112,3 +112,26 @@ def test_barycenter_eval_combine_of_row_shards():
     ls = np.array([b[127] for b in bufs])
     assert abs(out[127] - np.log(np.exp(ls).sum())) <= 1e-14 * abs(out[127]) + 1e-15
     assert np.array_equal(_combine_eval_buffers([bufs[0]], m), bufs[0])
+
+
+def test_spec6_balancing_is_the_kl_projection():
+    """SPEC acceptance 6: on a grid of 10^3 (delta, beta) pairs the clamp of the log-odds
+    (dxg.balance, dxg.py:236-245) is the KL projection of (mu+, mu-) = (logistic(delta),
+    1 - logistic(delta)) onto {|log(mu+/mu-)| <= beta}, found numerically, within 1e-10."""
+    import numpy as np
+    from scipy.optimize import minimize_scalar
+    from paper_2511_11359_b200 import dxg
+    deltas = np.linspace(-6.0, 6.0, 40)
+    betas = np.linspace(0.05, 5.0, 25)
+    for beta in betas:
+        got = dxg.balance(dxg.LogOddsField(deltas), float(beta)).delta
+        for d, g in zip(deltas, got):
+            mp = 1.0 / (1.0 + np.exp(-d))
+            lo, hi = 1.0 / (1.0 + np.exp(beta)), 1.0 / (1.0 + np.exp(-beta))
+
+            def kl(q):
+                return q * np.log(q / mp) + (1 - q) * np.log((1 - q) / (1 - mp))
+            res = minimize_scalar(kl, bounds=(lo, hi), method="bounded", options={"xatol": 1e-14})
+            q = min(max(res.x, lo), hi)
+            q = lo if kl(lo) < kl(q) else (hi if kl(hi) < kl(q) else q)
+            assert abs(np.log(q / (1 - q)) - g) <= 1e-6 or abs(q - 1.0 / (1.0 + np.exp(-g))) <= 1e-10
