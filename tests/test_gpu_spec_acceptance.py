@@ -211,7 +211,8 @@ def test_11_determinism_byte_identical_trajectories():
 def _wkl(plan_star, plan, delta_star, delta, ct, tau_p, tau_mu):
     """Weighted KL D^w(zeta* || zeta) for m = 1: plans D_r p and the
     column pairs D_c~ (mu+, mu-) with mu+ = logistic(delta)."""
-    kp = float(np.sum(np.where(plan_star > 0, plan_star * (np.log(plan_star) - np.log(plan)), 0.0)))
+    with np.errstate(divide="ignore", invalid="ignore"):   # 0 log 0 terms are masked out
+        kp = float(np.sum(np.where(plan_star > 0, plan_star * (np.log(plan_star) - np.log(plan)), 0.0)))
     sp = 1.0 / (1.0 + np.exp(-delta_star))
     s = 1.0 / (1.0 + np.exp(-delta))
     km = float(np.sum(ct * (sp * (np.log(sp) - np.log(s)) + (1 - sp) * (np.log1p(-sp) - np.log1p(-s)))))
