@@ -457,7 +457,7 @@ def solve(kernel: CostKernel, r: Histogram, c: Histogram, params: DxgParams,
             eng.sweep(evaluate=True)
             swept = True
         primal, dual, infeas = eng.evaluate()
-        s_val = eng.scalars()[2]
+        s_val = eng.last_scalars[2]      # read with the evaluation buffer (one transfer)
         point = TrajectoryPoint(it, time.perf_counter() - t0, primal, dual, primal - dual, infeas, s_val)
         trajectory.append(point)
         return point

@@ -218,11 +218,17 @@ class DxgEngine:
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_eval(C.byref(self.plan), self._stream()), "dxg_eval")
         buf = self.evalbuf[:5]
+        # the scalars (a, a_bar, s, t) travel in the same device->host transfer
+        self.evalbuf[8:12].copy_(self.scal[:4])
         if self.world > 1:
             cost_v, ent_rows, inner_rows = combine_partials(buf[:3], self.group, self.world).cpu().tolist()
-            infeas, cd = buf[3:5].cpu().tolist()
+            tail = self.evalbuf[3:12].cpu().tolist()
+            infeas, cd = tail[0], tail[1]
+            self.last_scalars = tail[5:9]
         else:
-            cost_v, ent_rows, inner_rows, infeas, cd = buf.cpu().tolist()
+            vals = self.evalbuf[:12].cpu().tolist()
+            cost_v, ent_rows, inner_rows, infeas, cd = vals[:5]
+            self.last_scalars = vals[8:12]
         eta = self.params.eta
         sup = self.kernel.sup_norm
         ent = ent_rows + self.h_r
