@@ -169,6 +169,12 @@ int leanot_dxg_update(const leanot_dxg_plan_t* plan, void* stream);
 int leanot_dxg_eval(const leanot_dxg_plan_t* plan, void* stream);
 /* iters x (sweep, update) -- capturable; single process only */
 int leanot_dxg_iterate(const leanot_dxg_plan_t* plan, int iters, void* stream);
+/* One logging interval of solve() in one launch (small single-process plans, n <= 1024):
+ * [leanot_dxg_update from the marginals of the last sweep if start_update] + the rest of
+ * `iters` updates as full iterations + the evaluation sweep of the final state, i.e. the
+ * sequence update / iterate / sweep(EVAL) / eval; evalbuf[0..4] as leanot_dxg_eval and
+ * evalbuf[8..11] = (a, a_bar, s, t).  Returns LEANOT_EINVAL for plans it does not cover. */
+int leanot_dxg_iterate_eval(const leanot_dxg_plan_t* plan, int iters, int start_update, void* stream);
 /* CUDA graph of `iters` plain iterations (captured once, replayed) */
 int leanot_graph_create(const leanot_dxg_plan_t* plan, int iters, void** graph_exec, void* stream);
 int leanot_graph_launch(void* graph_exec, void* stream);

@@ -77,6 +77,7 @@ def lib():
         "leanot_points_sup": ([vp, i64, C.c_int, C.c_int, vp, vp, vp], C.c_int),
         "leanot_points_norms": ([vp, i64, C.c_int, vp, vp], C.c_int),
         "leanot_sum_partials": ([vp, C.c_int, i64, vp, vp], C.c_int),
+        "leanot_dxg_iterate_eval": ([C.POINTER(DxgPlanT), C.c_int, C.c_int, vp], C.c_int),
         "leanot_bary_rows": ([C.POINTER(BaryPlanT), C.c_int, vp, vp], C.c_int),
         "leanot_bary_rnorm": ([C.POINTER(BaryPlanT), vp, vp, vp], C.c_int),
         "leanot_bary_cols": ([C.POINTER(BaryPlanT), vp, vp], C.c_int),
@@ -128,7 +129,7 @@ def lib():
 EXPORTS = (
     "leanot_version", "leanot_last_error", "leanot_device_sm_count", "leanot_dxg_default_splits",
     "leanot_cost_block", "leanot_stored_max", "leanot_stored_normalize", "leanot_points_sup", "leanot_points_norms", "leanot_sum_partials",
-    "leanot_bary_rows", "leanot_bary_rnorm", "leanot_bary_cols",
+    "leanot_bary_rows", "leanot_bary_rnorm", "leanot_bary_cols", "leanot_dxg_iterate_eval",
     "leanot_hash_fill", "leanot_sweep_ws_doubles", "leanot_column_marginals", "leanot_row_lse",
     "leanot_plan_stats", "leanot_row_min", "leanot_row_lse_affine", "leanot_dxg_prepare",
     "leanot_dxg_sweep", "leanot_dxg_update", "leanot_dxg_eval", "leanot_dxg_iterate",

@@ -40,6 +40,12 @@ struct PersistArgs {
   double* gmax;     // 2 x gridDim.x block maxima
   int splits, ntile, iters;
   int64_t rows_per;  // pass B rows per split
+  // row-owner kernel only: start from the marginals in U.col (the last sweep of the state),
+  // and/or finish with an evaluation sweep of the final state (evalbuf as leanot_dxg_eval)
+  int start_update, eval;
+  double eta;
+  double* evalbuf;
+  double* epart;     // gridDim.x x 5 per-CTA evaluation partials
 };
 
 __device__ __forceinline__ double block_max_bcast(double v, double* red) {
@@ -319,12 +325,13 @@ __global__ void __launch_bounds__(PS_THREADS) dxg_persist_kernel(const PersistAr
 //   the previous iteration, exact-max recompute of out-of-range rows) and fixed reduction
 //   orders; the column sums are sum_i g_i e_ij with the product formed after the exp
 //   (the regular pass B folds g into the polynomial: same value to a few ulps).
-constexpr int PO_THREADS = 512;            // 16 warps: latency hiding for the exp chains
+constexpr int PO_THREADS = 256;            // 8 warps, 255-register budget for the exps held in registers
 constexpr int PO_WARPS = PO_THREADS / 32;
-constexpr int PO_J = 2;                    // columns per thread (n <= 1024)
+constexpr int PO_J = 4;                    // columns per thread (n <= 1024)
 constexpr int PO_R = 8;                    // max rows per CTA
 constexpr int64_t PO_MAX_N = PO_THREADS * PO_J;
-constexpr int PO_PARTS = 6;                // partials per lane in the column sums (G <= 192)
+constexpr int PO_LPV = PO_THREADS / 16;    // lanes per value in the column sums (16 values)
+constexpr int PO_PARTS = 12;               // partials per lane in the column sums (G <= 192)
 
 __device__ __forceinline__ double po_block_max(double v, double* red) {
   v = warp_max(v);
@@ -413,8 +420,14 @@ __global__ void __launch_bounds__(PO_THREADS, 1) dxg_rowowner_kernel(const Persi
   double d_o = owner ? U.delta[jo] : 0.0;
   __syncthreads();
 
-  for (int it = 0; it < P.iters; ++it) {
+  for (int it = 0; it <= P.iters; ++it) {
+    const bool last = it == P.iters;  // the evaluation sweep of the final state (if requested)
+    if (last && !P.eval) break;
     const double na[2] = {-sc[0], -sc[1]};
+    double cn_o = 0.0, cb_o = 0.0;    // owner: the column's two marginals
+    if (it == 0 && P.start_update) {
+      if (owner) { cn_o = U.col[jo]; cb_o = U.col[n + jo]; }
+    } else {
     PO_TS(0);
     // ---- pass A on the own rows; exps kept in registers ----
     double e[PO_R][PO_J][2], s[PO_R][2];
@@ -538,12 +551,61 @@ __global__ void __launch_bounds__(PO_THREADS, 1) dxg_rowowner_kernel(const Persi
         P.slab[((int64_t)c * 2 + 1) * n + j] = a1;
       }
     }
+    if (last) {  // after pass B: the register-resident exps are dead here
+      // evaluation statistics of weight set 0 over the own rows (rowpass EVAL + eval kernels):
+      // <C, D_r p>, sum_i r_i H(p_i) and sum_i r_i v_i with v_i = min_j (C_ij + sd_j) (eta = 0,
+      // dxg.py:344-348) or LSE_j(-(C_ij + sd_j) / eta) (dxg.py:337); fixed orders
+      double rs0 = 0.0, rs1 = 0.0, rs2 = 0.0;
+#pragma unroll 1
+      for (int q = 0; q < nrow; ++q) {  // block-uniform
+        // the exps of weight set 0 recomputed with the shift pass A used (bitwise the same
+        // values; keeps the register-resident e[][][] statically indexed)
+        const uint32_t m0 = (uint32_t)smk[2 * q];
+        double uu = 0.0, vv = 0.0, mn = INFINITY;
+        for (int64_t j = threadIdx.x; j < n; j += PO_THREADS) {
+          const double cq = sC[q * n + j];
+          const double x0 = fma(na[0], cq, -sb[j]);
+          const double e0 = texp(tb, x0, m0);
+          uu = fma(e0, cq, uu);
+          vv = fma(e0, x0, vv);
+          mn = fmin(mn, cq + __ldcg(U.sd + j));
+        }
+        uu = po_block_sum(uu, red);
+        vv = po_block_sum(vv, red);
+        double v;
+        if (P.eta > 0) {
+          const double ie = -1.0 / P.eta;
+          double mx = -INFINITY;
+          for (int64_t j = threadIdx.x; j < n; j += PO_THREADS) mx = fmax(mx, (sC[q * n + j] + __ldcg(U.sd + j)) * ie);
+          mx = po_block_max(mx, red);
+          double t = 0.0;
+          for (int64_t j = threadIdx.x; j < n; j += PO_THREADS) t += exp((sC[q * n + j] + __ldcg(U.sd + j)) * ie - mx);
+          t = po_block_sum(t, red);
+          v = mx + log(t);
+        } else {
+          v = po_block_max(-mn, red);
+          v = -v;
+        }
+        double rq = rw[0];
+#pragma unroll
+        for (int qq = 1; qq < PO_R; ++qq) rq = q == qq ? rw[qq] : rq;
+        const double S0 = sS[2 * q];
+        rs0 += (rq / S0) * uu;
+        if (rq > 0.0) rs1 += rq * (((double)smk[2 * q] * LSTEP + log(S0)) - vv / S0);
+        rs2 += rq * v;
+      }
+      if (threadIdx.x == 0) {
+        P.epart[c * 5 + 0] = rs0;
+        P.epart[c * 5 + 1] = rs1;
+        P.epart[c * 5 + 2] = rs2;
+      }
+    }
     PO_TS(3);
     grid.sync();
     PO_TS(4);
     // ---- owned columns: fixed-order sum of the partials (16 lanes per value), updates ----
     {
-      const int v = threadIdx.x >> 5, part = threadIdx.x & 31;  // value v = 2 * column + set
+      const int v = threadIdx.x / PO_LPV, part = threadIdx.x % PO_LPV;  // value v = 2 * column + set
       double t = 0.0;
       if (v < 2 * ncol) {
         // all of this lane's partials in flight at once, then added in order
@@ -551,23 +613,48 @@ __global__ void __launch_bounds__(PO_THREADS, 1) dxg_rowowner_kernel(const Persi
         double pv[PO_PARTS];
 #pragma unroll
         for (int u = 0; u < PO_PARTS; ++u) {
-          const int p = part + 32 * u;
+          const int p = part + PO_LPV * u;
           pv[u] = p < grows ? __ldcg(P.slab + ((int64_t)p * 2 + (v & 1)) * n + j) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < PO_PARTS; ++u) t += pv[u];
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      for (int o = PO_LPV / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
       if (part == 0 && v < 16) scol[v] = t;
     }
     __syncthreads();
+    if (owner) {
+      cn_o = scol[2 * threadIdx.x];
+      cb_o = scol[2 * threadIdx.x + 1];
+      const_cast<double*>(U.col)[jo] = cn_o;
+      const_cast<double*>(U.col)[n + jo] = cb_o;
+    }
+    }  // sweep of this step
+    if (last) {
+      // column statistics of the swept state (colstats_reduce_kernel), then the fixed-order
+      // combination of the per-CTA partials by CTA 0
+      double s3 = owner ? fabs(cn_o - c_o) : 0.0;
+      double s4 = owner ? c_o * tanh(0.5 * d_o) : 0.0;
+      s3 = po_block_sum(s3, red);
+      s4 = po_block_sum(s4, red);
+      if (threadIdx.x == 0) {
+        P.epart[c * 5 + 3] = s3;
+        P.epart[c * 5 + 4] = s4;
+      }
+      grid.sync();
+      if (c == 0 && threadIdx.x < 5) {
+        double t = 0.0;
+        for (int q = 0; q < G; ++q) t += __ldcg(P.epart + q * 5 + threadIdx.x);
+        P.evalbuf[threadIdx.x] = t;
+      }
+      if (c == 0 && threadIdx.x < 4) P.evalbuf[8 + threadIdx.x] = sc[threadIdx.x];
+      break;
+    }
     double mx = -INFINITY;
     if (owner) {
       const int64_t j = jo;
-      const double cn = scol[2 * threadIdx.x], cb = scol[2 * threadIdx.x + 1];
-      const_cast<double*>(U.col)[j] = cn;
-      const_cast<double*>(U.col)[n + j] = cb;
+      const double cn = cn_o, cb = cb_o;
       const double dbar = md_step(U.A, U.B, d_o, cn, c_o, ct_o);
       double dn = md_step(U.A, U.B, d_o, cb, c_o, ct_o);
       dn = fmin(fmax(dn, -U.beta), U.beta);
@@ -654,12 +741,13 @@ struct RowOwnerFn {
     PersistArgs a = P;
     const int64_t n = a.U.n;
     const int G = num_sms();
-    if ((n + G - 1) / G > PO_R || n > PO_MAX_N || G > 32 * PO_PARTS) return LEANOT_EINVAL;
-    if ((int64_t)G * 2 * n + G > slab_doubles) return LEANOT_EINVAL;
+    if ((n + G - 1) / G > PO_R || n > PO_MAX_N || G > PO_LPV * PO_PARTS) return LEANOT_EINVAL;
+    if ((int64_t)G * 2 * n + 6 * G > slab_doubles) return LEANOT_EINVAL;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PO_THREADS, smem) != cudaSuccess || occ < 1)
       return LEANOT_EINVAL;
     a.gmax = a.slab + (int64_t)G * 2 * n;
+    a.epart = a.gmax + G;
     void* args[] = {&a};
     const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, G, PO_THREADS, args, smem, st);
     if (e != cudaSuccess) {
@@ -751,12 +839,38 @@ static int try_persist_iterate(const leanot_dxg_plan_t& P, int iters, cudaStream
   A.splits = 0;
   A.ntile = (int)((n + 31) / 32);
   A.iters = iters;
+  A.start_update = 0; A.eval = 0; A.eta = P.prm.eta; A.evalbuf = P.evalbuf; A.epart = nullptr;
   if (n <= PO_MAX_N && rowowner_env()) {
     RowOwnerFn g{A, (int64_t)P.splits * 2 * n, st};
     if (LEANOT_DISPATCH_COST(A.cost, g) == LEANOT_OK) return LEANOT_OK;
   }
   PersistFn f{A, 2, P.splits, (size_t)(TAB_BYTES + ((n + 1) & ~int64_t(1)) * 8), st};
   return LEANOT_DISPATCH_COST(A.cost, f);
+}
+
+// Interval of solve() (dxg.py:420-472) between two logging points in ONE launch:
+// [update from the marginals in U.col when start_update] + the remaining of `iters` updates
+// as full iterations + the evaluation sweep of the final state (evalbuf[0..4] as
+// leanot_dxg_eval, evalbuf[8..11] = a, a_bar, s, t; U.col = its marginals).  Row-owner
+// plans only (single process, n <= 1024, not the separable path); LEANOT_EINVAL otherwise.
+static int try_rowowner_iterate_eval(const leanot_dxg_plan_t& P, int iters, int start_update, cudaStream_t st) {
+  if (!persist_env() || !rowowner_env() || iters < 0 || P.n > PO_MAX_N || P.row0 != 0 || P.row1 != P.n ||
+      use_sep(P))
+    return LEANOT_EINVAL;
+  if (iters == 0 && start_update) return LEANOT_EINVAL;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return LEANOT_EINVAL;
+  const int64_t n = P.n;
+  PersistArgs A;
+  memset(&A, 0, sizeof(A));
+  A.cost = make_view(P.cost);
+  A.U = make_upd(P);
+  A.r = P.r; A.shift = P.shift; A.m = P.m; A.S = P.S; A.coef = P.coef; A.slab = P.slab;
+  A.ntile = (int)((n + 31) / 32);
+  A.iters = iters;
+  A.start_update = start_update; A.eval = 1; A.eta = P.prm.eta; A.evalbuf = P.evalbuf;
+  RowOwnerFn g{A, (int64_t)P.splits * 2 * n, st};
+  return LEANOT_DISPATCH_COST(A.cost, g);
 }
 
 }  // namespace leanot

@@ -518,6 +518,7 @@ static int sep_dxg_sweep(const leanot_dxg_plan_t& P, bool eval, cudaStream_t st)
 static int sep_dxg_eval(const leanot_dxg_plan_t& P, cudaStream_t st);
 // persistent small-n iterations (leanot_persist.cu)
 static int try_persist_iterate(const leanot_dxg_plan_t& P, int iters, cudaStream_t st);
+static int try_rowowner_iterate_eval(const leanot_dxg_plan_t& P, int iters, int start_update, cudaStream_t st);
 // single-launch L2-reuse sweep for stored costs (leanot_fused.cu)
 static int try_fused_sweep(const leanot_dxg_plan_t& P, cudaStream_t st);
 static bool fused_default();
@@ -924,6 +925,17 @@ int leanot_dxg_iterate(const leanot_dxg_plan_t* P, int iters, void* stream) {
     LEANOT_TRY(leanot_dxg_update(P, stream));
   }
   return LEANOT_OK;
+}
+
+int leanot_dxg_iterate_eval(const leanot_dxg_plan_t* P, int iters, int start_update, void* stream) {
+  LEANOT_TRY(validate_plan(P));
+  LEANOT_TRY(ensure_init());
+  const int rc = try_rowowner_iterate_eval(*P, iters, start_update, S_(stream));
+  if (rc != LEANOT_OK) {
+    set_error("dxg_iterate_eval: plan not eligible (single-process, n <= 1024, non-separable cost)");
+    return rc;
+  }
+  return check_launch("dxg_iterate_eval");
 }
 
 int leanot_graph_create(const leanot_dxg_plan_t* P, int iters, void** graph_exec, void* stream) {

@@ -462,7 +462,29 @@ def solve(kernel: CostKernel, r: Histogram, c: Histogram, params: DxgParams,
         trajectory.append(point)
         return point
 
-    while it < max_iter:
+    # small single-process plans: one launch per logging interval (update + iterations +
+    # evaluation sweep, leanot_dxg_iterate_eval) and one device->host read
+    folded = timeout is None and eng.world == 1 and n <= 1024
+    while folded and it < max_iter:
+        nxt = min(((it // log_stride) + 1) * log_stride, max_iter)
+        with torch.cuda.device(eng.device):
+            rc = _lib.lib().leanot_dxg_iterate_eval(C.byref(eng.plan), int(nxt - it), 1 if swept else 0,
+                                                    _lib.stream_handle())
+        if rc != _lib.LEANOT_OK:
+            if it == 0 and not swept:
+                folded = False          # not eligible (e.g. separable grid path): regular loop
+                break
+            _lib.check(rc, "dxg_iterate_eval")
+        it = nxt
+        swept = True
+        primal, dual, infeas = eng.evaluate_buffer()
+        point = TrajectoryPoint(it, time.perf_counter() - t0, primal, dual, primal - dual, infeas,
+                                eng.last_scalars[2])
+        trajectory.append(point)
+        if point.gap <= termination.eps / 6.0 and point.col_infeas_l1 <= termination.eps / 6.0:
+            converged = True
+            break
+    while not folded and it < max_iter:
         if timeout is None:
             # run to the next logging point without host syncs:
             # update (uses the swept marginals) + k x (sweep, update)

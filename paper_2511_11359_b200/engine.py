@@ -217,9 +217,14 @@ class DxgEngine:
         torch = _torch()
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_eval(C.byref(self.plan), self._stream()), "dxg_eval")
-        buf = self.evalbuf[:5]
         # the scalars (a, a_bar, s, t) travel in the same device->host transfer
         self.evalbuf[8:12].copy_(self.scal[:4])
+        return self.evaluate_buffer()
+
+    def evaluate_buffer(self):
+        """(primal, dual, infeas) from evalbuf[0..4] (+ scalars in [8..11]) as filled by
+        leanot_dxg_eval or leanot_dxg_iterate_eval."""
+        buf = self.evalbuf[:5]
         if self.world > 1:
             cost_v, ent_rows, inner_rows = combine_partials(buf[:3], self.group, self.world).cpu().tolist()
             tail = self.evalbuf[3:12].cpu().tolist()
