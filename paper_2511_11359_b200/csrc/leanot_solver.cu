@@ -601,8 +601,8 @@ int leanot_dxg_default_splits(int64_t n, int64_t rows, int* out) {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (n + 1023) / 1024;   // column-pass tile = 1024 columns
   const int64_t smax = std::min<int64_t>(64, std::max<int64_t>(1, rows / 8));
-  if (n <= 16384) {
-    // small plans: the column pass is a few waves of (tile, split) items over the 2 x SMs
+  if (n <= 16384 || n >= 262144) {
+    // small plans and very large ones: the column pass is a few waves of (tile, split) items over the 2 x SMs
     // resident CTAs, so pick the split count whose items fill the last wave best (fewest
     // items among the best); at n = 1e4 this is 29 splits = 290 items in one wave, 11 %
     // faster than 64 splits = 2.16 waves (tools/splits_sweep.py)
@@ -611,7 +611,10 @@ int leanot_dxg_default_splits(int64_t n, int64_t rows, int* out) {
       const int64_t items = tiles * s;
       return (double)items / (double)(((items + G - 1) / G) * G);
     };
-    auto eligible = [&](int64_t s) { return tiles * s >= (G * 9) / 10 || s == smax; };  // >= ~one wave
+    // >= ~one wave for small n; >= 3 waves for the large on-the-fly shards (BASELINE config 4:
+    // 3 splits = 9.9 waves, pass B 5 % faster than 2 splits = 6.6 waves)
+    const int64_t min_items = n <= 16384 ? (G * 9) / 10 : 3 * G;
+    auto eligible = [&](int64_t s) { return tiles * s >= min_items || s == smax; };
     double best_eff = 0.0;
     for (int64_t s = 1; s <= smax; ++s)
       if (eligible(s)) best_eff = std::max(best_eff, eff_of(s));

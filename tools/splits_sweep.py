@@ -15,7 +15,13 @@ from paper_2511_11359_b200.engine import DxgEngine  # noqa: E402
 kind, n = sys.argv[1], int(sys.argv[2])
 splits_list = [int(x) for x in sys.argv[3].split(",")]
 rng = np.random.default_rng(1)
-k = core.HashKernel(n, seed=0) if kind == "hash" else core.ColorKernel(rng.random((n, 2)), 2, scale=2.0)
+if kind == "hash":
+    k = core.HashKernel(n, seed=0)
+elif kind == "points3shard":   # BASELINE config 4: a 1/8 row shard of n 3-D points
+    k = core.ColorKernel(rng.random((n, 3)), 2, scale=3.0)
+    k.row0, k.row1 = 0, n // 8
+else:
+    k = core.ColorKernel(rng.random((n, 2)), 2, scale=2.0)
 r = rng.random(n); r /= r.sum()
 c = rng.random(n); c /= c.sum()
 for s in splits_list:
@@ -24,7 +30,7 @@ for s in splits_list:
     for _ in range(3):
         eng.sweep(); eng.update()
     tb = []
-    reps = 5 if n >= 50000 else 50
+    reps = 3 if n >= 50000 else 50
     for _ in range(reps):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(); eng.sweep_phase("rows"); e[1].record(); eng.sweep_phase("cols"); e[2].record()
