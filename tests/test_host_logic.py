@@ -135,3 +135,28 @@ def test_spec6_balancing_is_the_kl_projection():
             q = min(max(res.x, lo), hi)
             q = lo if kl(lo) < kl(q) else (hi if kl(hi) < kl(q) else q)
             assert abs(np.log(q / (1 - q)) - g) <= 1e-6 or abs(q - 1.0 / (1.0 + np.exp(-g))) <= 1e-10
+
+
+def test_default_splits_fill_the_waves():
+    """leanot_dxg_default_splits (no GPU: 148 SMs assumed): small and very large plans pick the
+    column-pass split count whose (tile, split) items fill the last wave over 2 x 148 resident
+    CTAs (fewest items within 2 % of the best fill); mid sizes keep >= 4 items per CTA."""
+    import ctypes
+    from paper_2511_11359_b200 import _lib
+    L = _lib.lib()
+
+    def splits(n, rows):
+        s = ctypes.c_int(0)
+        assert L.leanot_dxg_default_splits(n, rows, ctypes.byref(s)) == 0
+        return s.value
+
+    def fill(n, s):
+        items = ((n + 1023) // 1024) * s
+        return items / (-(-items // 296) * 296)
+
+    assert splits(10_000, 10_000) == 29 and fill(10_000, 29) > 0.97          # config 2: one full wave
+    assert splits(1_000_000, 125_000) == 3 and fill(1_000_000, 3) > 0.98     # config 4 shard
+    assert splits(100_000, 100_000) == 19                                    # config 3 (measured)
+    for n in (2000, 5000, 16384):
+        s = splits(n, n)
+        assert 1 <= s <= 64 and s <= max(1, n // 8)
