@@ -247,3 +247,32 @@ def test_persistent_iterations_match_launch_per_kernel_path(kind, n):
     (d0, b0, a0, s0, t0), (d1, b1, a1, s1, t1) = out
     assert rel_err(d0, d1) <= 1e-11 and rel_err(b0, b1) <= 1e-11
     assert a0 == a1 and s0 == s1 and t0 == t1 == 110
+
+
+@pytest.mark.parametrize("n", [500, 2000])
+def test_persistent_paths_recompute_out_of_range_rows(n):
+    """A jump in a after the shifts were set (every row sum far outside [2^-900, 2^900]) forces
+    the exact-max recompute inside the persistent kernels (row-owner for n <= 1024, the
+    four-barrier one above): they must track the launch-per-kernel path."""
+    dxg = _dxg()
+    from paper_2511_11359_b200 import core
+    from paper_2511_11359_b200.engine import DxgEngine
+    rng = np.random.default_rng(n + 7)
+    k = core.ExplicitKernel(rng.random((n, n)))
+    r, c = O.normalized_hist(rng.random(n)), O.normalized_hist(rng.random(n))
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    delta = rng.uniform(-1, 1, n)
+    b = -np.abs(rng.normal(0, 5, n))
+    b -= b.max()
+    out = []
+    for graph in (False, True):
+        eng = DxgEngine(k, r, c, prm)
+        eng.load_state(delta, b, 10.0, 0.0, 10)
+        eng.scal[0] = 2500.0
+        eng.scal[1] = 2500.0 + prm.tau_p
+        eng.iterate(6, use_graph=graph)
+        out.append(eng.read_state())
+    (d0, b0, a0, s0, t0), (d1, b1, a1, s1, t1) = out
+    assert np.all(np.isfinite(d0)) and np.all(np.isfinite(b0))
+    assert rel_err(d0, d1) <= 1e-11 and rel_err(b0, b1) <= 1e-11
+    assert a0 == a1 and t0 == t1 == 16
