@@ -268,8 +268,8 @@ def test_persistent_paths_recompute_out_of_range_rows(n):
     for graph in (False, True):
         eng = DxgEngine(k, r, c, prm)
         eng.load_state(delta, b, 10.0, 0.0, 10)
-        eng.scal[0] = 2500.0
-        eng.scal[1] = 2500.0 + prm.tau_p
+        eng.scal[0] = 1.0e6                  # x - m ~ -1e6 min_j C_ij: row sums underflow
+        eng.scal[1] = 1.0e6 + prm.tau_p
         eng.iterate(6, use_graph=graph)
         out.append(eng.read_state())
     (d0, b0, a0, s0, t0), (d1, b1, a1, s1, t1) = out
