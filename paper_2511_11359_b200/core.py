@@ -24,7 +24,8 @@ import numpy as np
 from . import _lib
 
 __all__ = ["DENSE_CAP", "BLOCK_ROWS", "Histogram", "CostKernel", "GridKernel", "ExplicitKernel",
-           "ColorKernel", "HashKernel", "cost_eval", "iter_blocks"]
+           "ColorKernel", "HashKernel", "cost_eval", "iter_blocks", "ingest_image_histogram", "lse",
+           "lse_rows", "kl_divergence", "entropy", "logistic"]
 
 DENSE_CAP = 4096      # core.py:40
 BLOCK_ROWS = 128      # core.py:44 (the GPU sweeps do not use host row blocks)
@@ -68,6 +69,80 @@ class Histogram:
 
     def min(self) -> float:
         return float(self.weights.min())
+
+
+def ingest_image_histogram(pixels, perturbation: float = 1e-6) -> Histogram:
+    """Grayscale image -> full-support row-major histogram (core.py:147-164).
+
+    Unit-mass normalization, + `perturbation` per pixel, renormalized; with a
+    zero perturbation exact zeros are kept (full_support False).  Same checks
+    and ValueError messages as the reference.
+    """
+    img = np.asarray(pixels, dtype=float)
+    if np.any(img < 0):
+        raise ValueError("image has negative pixels")
+    total = img.sum()
+    if total <= 0:
+        raise ValueError("image has no positive pixel")
+    h = img.ravel(order="C") / total
+    if perturbation != 0.0:
+        h = h + perturbation
+        h = h / h.sum()
+    return Histogram(h)
+
+
+# O(n) host helpers of the reference's public core surface (core.py:49-103).  The solvers
+# never call them on the n^2 path (their LSEs / entropies run in the CUDA sweeps); they are
+# here so user code importing them from leanot.core keeps working.
+
+def lse(values) -> float:
+    """Max-shifted log-sum-exp of a 1-D sequence (core.py:49-64); all -inf -> -inf."""
+    v = np.asarray(values, dtype=float)
+    if v.size == 0:
+        raise ValueError("lse of an empty sequence")
+    m = v.max()
+    if not np.isfinite(m):
+        if m == -np.inf:
+            return -np.inf
+        raise ValueError("lse input contains +inf or NaN")
+    return float(m + np.log(np.exp(v - m).sum()))
+
+
+def lse_rows(z) -> np.ndarray:
+    """Row-wise log-sum-exp of a 2-D array (core.py:67-70)."""
+    z = np.asarray(z, dtype=float)
+    m = z.max(axis=1)
+    return m + np.log(np.exp(z - m[:, None]).sum(axis=1))
+
+
+def kl_divergence(a, b) -> float:
+    """<a, log a - log b>, 0 log 0 = 0; a must be absolutely continuous w.r.t. b (core.py:73-86)."""
+    a = np.asarray(a, dtype=float).ravel()
+    b = np.asarray(b, dtype=float).ravel()
+    if a.shape != b.shape:
+        raise ValueError("kl_divergence: shape mismatch")
+    pos = a > 0
+    if np.any(b[pos] <= 0):
+        raise ValueError("kl_divergence: a is not absolutely continuous w.r.t. b")
+    return float(np.sum(a[pos] * (np.log(a[pos]) - np.log(b[pos]))))
+
+
+def entropy(weights) -> float:
+    """-sum x log x with 0 log 0 = 0 (core.py:89-93)."""
+    x = np.asarray(weights, dtype=float).ravel()
+    pos = x > 0
+    return float(-np.sum(x[pos] * np.log(x[pos])))
+
+
+def logistic(x) -> np.ndarray:
+    """Overflow-free elementwise sigmoid (core.py:96-104)."""
+    x = np.asarray(x, dtype=float)
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    ex = np.exp(x[~pos])
+    out[~pos] = ex / (1.0 + ex)
+    return out
 
 
 def as_weights(h) -> np.ndarray:

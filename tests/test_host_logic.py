@@ -160,3 +160,31 @@ def test_default_splits_fill_the_waves():
     for n in (2000, 5000, 16384):
         s = splits(n, n)
         assert 1 <= s <= 64 and s <= max(1, n // 8)
+
+
+def _core_cases():
+    import json
+    from pathlib import Path
+    z = np.load(Path(__file__).parent / "golden" / "core_cases.npz")
+    meta = json.loads(bytes(z["__meta__"]).decode())
+    return z, meta
+
+
+@pytest.mark.parametrize("name", sorted(_core_cases()[1]))
+def test_core_helpers_match_reference(name):
+    """Reference leanot.core helpers (core.py:49-164) replayed from oracle/gen_golden_core.py."""
+    from paper_2511_11359_b200 import core
+    z, meta = _core_cases()
+    rec = meta[name]
+    args = [z[f"{name}__arg{q}"] for q in range(rec["nargs"])]
+    fn = getattr(core, rec["fn"])
+    if rec["kind"] == "error":
+        with pytest.raises(Exception) as ei:
+            fn(*args, **rec["kw"])
+        assert type(ei.value).__name__ == rec["exc"] and str(ei.value) == rec["msg"]
+        return
+    out = fn(*args, **rec["kw"])
+    if rec["kind"] == "histogram":
+        assert out.full_support == rec["full_support"]
+        out = out.weights
+    np.testing.assert_array_equal(np.asarray(out, dtype=float), z[f"{name}__out"])
