@@ -24,7 +24,7 @@ import numpy as np
 from . import _lib
 
 __all__ = ["DENSE_CAP", "BLOCK_ROWS", "Histogram", "CostKernel", "GridKernel", "ExplicitKernel",
-           "ColorKernel", "HashKernel", "cost_eval", "iter_blocks", "ingest_image_histogram", "lse",
+           "ColorKernel", "HashKernel", "cost_eval", "iter_blocks", "map_blocks", "ingest_image_histogram", "lse",
            "lse_rows", "kl_divergence", "entropy", "logistic"]
 
 DENSE_CAP = 4096      # core.py:40
@@ -204,6 +204,22 @@ def cost_eval(kernel: CostKernel, i: int, j: int) -> float:
 def iter_blocks(n: int, block_rows: int = BLOCK_ROWS):
     for i0 in range(0, n, block_rows):
         yield i0, min(i0 + block_rows, n)
+
+
+def map_blocks(fn, n: int, workers: int = 1, block_rows: int = BLOCK_ROWS) -> list:
+    """fn(i0, i1) over the row blocks, results in block order (core.py:297-309).
+
+    Kept for user plug-ins that stream `block()`; the CUDA solvers never call it (their
+    row blocks are CTAs, reduced in a fixed order on device).  With workers > 1 the
+    blocks run on a thread pool but are consumed in block order (deterministic).
+    """
+    ranges = list(iter_blocks(n, block_rows))
+    if workers <= 1 or len(ranges) == 1:
+        return [fn(i0, i1) for i0, i1 in ranges]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        futures = [pool.submit(fn, i0, i1) for i0, i1 in ranges]
+        return [f.result() for f in futures]
 
 
 def _even(n: int) -> int:

@@ -188,3 +188,9 @@ def test_core_helpers_match_reference(name):
         assert out.full_support == rec["full_support"]
         out = out.weights
     np.testing.assert_array_equal(np.asarray(out, dtype=float), z[f"{name}__out"])
+
+
+def test_map_blocks_block_order():
+    from paper_2511_11359_b200.core import map_blocks
+    for w in (1, 3):
+        assert map_blocks(lambda i0, i1: (i0, i1), 300, workers=w) == [(0, 128), (128, 256), (256, 300)]
