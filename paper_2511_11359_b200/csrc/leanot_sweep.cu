@@ -31,6 +31,9 @@ namespace leanot {
 #ifndef LEANOT_RP_MINB
 #define LEANOT_RP_MINB 2  // pass-A CTAs per SM the register budget targets
 #endif
+#ifndef LEANOT_CP_SROW
+#define LEANOT_CP_SROW 1  // pass B, on-the-fly costs: row data staged in shared memory per chunk
+#endif
 #ifndef LEANOT_CP_MINB
 #define LEANOT_CP_MINB 2  // pass-B CTAs per SM the register budget targets
 #endif
@@ -332,6 +335,9 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
   extern __shared__ __align__(16) char smem[];
   double* s_coef = reinterpret_cast<double*>(smem + TAB_BYTES);            // [CP_CHUNK][K][4]
   uint32_t* s_m = reinterpret_cast<uint32_t*>(s_coef + CP_CHUNK * K * 4);  // [CP_CHUNK][K]
+  // on-the-fly costs: the chunk's row data (features / grid coordinates) staged with the
+  // row constants, so the inner loop reads it as shared-memory broadcasts
+  typename COST::Row* s_row = reinterpret_cast<typename COST::Row*>(s_m + CP_CHUNK * K);  // [CP_CHUNK]
   load_table(reinterpret_cast<double*>(smem));
   __syncthreads();
   const uint32_t tb = lane_tab_addr(smem);
@@ -374,6 +380,8 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
         int q = t / K, k = t % K;
         s_m[t] = (uint32_t)A.m[k * nr + (q0 - A.i0 + q)];
       }
+      if constexpr (!COST::kStored && LEANOT_CP_SROW)
+        for (int t = threadIdx.x; t < nq; t += CP_THREADS) s_row[t] = cost.row(q0 + t);
       __syncthreads();
       if (full) {
         // 2-row ping-pong: rows (q, q+1) compute while rows (q+2, q+3) load
@@ -382,6 +390,7 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
         auto fetch = [&](typename COST::Pre4& p, int q) {
           if (q < nq) {
             if constexpr (COST::kStored) cost.pre4(row, j, p);
+            else if constexpr (LEANOT_CP_SROW) cost.pre4(s_row[q], j, p);
             else cost.pre4(cost.row(q0 + q), j, p);
           }
           if constexpr (COST::kStored) row.p += cost.ld;
@@ -705,7 +714,7 @@ int launch_rowmax(const RowPassArgs& A, int K, int64_t* out, cudaStream_t st) {
 template <class COST, int K>
 static int launch_colpass_t(const ColPassArgs& A, cudaStream_t st) {
   auto kern = colpass_kernel<COST, K>;
-  const int smem = TAB_BYTES + CP_CHUNK * K * 4 * 8 + CP_CHUNK * K * 4;
+  const int smem = TAB_BYTES + CP_CHUNK * K * 4 * 8 + CP_CHUNK * K * 4 + (int)(CP_CHUNK * sizeof(typename COST::Row));
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return LEANOT_ECUDA;
