@@ -51,7 +51,7 @@ typedef struct leanot_cost {
   int64_t ld;         /* STORED row stride in doubles (>= n) */
   int64_t row_base;   /* STORED: global index of the first row held in mat */
   const double* mat;          /* STORED */
-  const double* feat;         /* POINTS: n x dim row-major */
+  const double* feat;         /* POINTS: n x dim row-major, 16-byte aligned */
   const double* grid_coords;  /* GRID: [row index (n) | column index (n)] as doubles */
   double inv_scale;   /* 1/scale for on-the-fly kinds */
   double sup_norm;    /* ||C||_inf after normalization: 1 or 0 */

@@ -64,6 +64,23 @@ struct CostStored {
   }
 };
 
+// Features of columns j, j+1 (j even, j + 1 < n) for the pass-A pipeline: the 2*DIM doubles
+// are contiguous and 16-byte aligned (row-major features; validate_cost requires a 16-byte
+// aligned base), so they arrive as DIM 16-byte loads instead of 2*DIM 8-byte ones.
+template <int DIM>
+__device__ __forceinline__ void col_pair(const double* f, int64_t j, double (&v0)[DIM], double (&v1)[DIM]) {
+  const double2* q = reinterpret_cast<const double2*>(f + j * DIM);
+  double e[2 * DIM];
+#pragma unroll
+  for (int t = 0; t < DIM; ++t) {
+    const double2 w = __ldg(q + t);
+    e[2 * t] = w.x;
+    e[2 * t + 1] = w.y;
+  }
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) { v0[d] = e[d]; v1[d] = e[DIM + d]; }
+}
+
 // ColorKernel: sum_d |f_id - f_jd|^P / scale (core.py:264-288)
 template <int DIM, int P>
 struct CostPoints {
@@ -121,7 +138,9 @@ struct CostPoints {
   }
   template <int R> struct Pre2 { Col c; };
   template <int R>
-  __device__ __forceinline__ void pre2(const Row (&)[R], const Col&, int64_t j, Pre2<R>& p) const { p.c = col(j); }
+  __device__ __forceinline__ void pre2(const Row (&)[R], const Col&, int64_t j, Pre2<R>& p) const {
+    col_pair<DIM>(f, j, p.c.v0, p.c.v1);
+  }
   template <int R>
   __device__ __forceinline__ void get2(const Row (&rows)[R], const Col&, const Pre2<R>& p, double (&c)[R][2]) const {
 #pragma unroll
@@ -199,7 +218,9 @@ struct CostGram {
   }
   template <int R> struct Pre2 { Col c; };
   template <int R>
-  __device__ __forceinline__ void pre2(const Row (&)[R], const Col&, int64_t j, Pre2<R>& p) const { p.c = col(j); }
+  __device__ __forceinline__ void pre2(const Row (&)[R], const Col&, int64_t j, Pre2<R>& p) const {
+    col_pair<DIM>(f, j, p.c.v0, p.c.v1);
+  }
   template <int R>
   __device__ __forceinline__ void get2(const Row (&rows)[R], const Col&, const Pre2<R>& p, double (&c)[R][2]) const {
 #pragma unroll

@@ -554,8 +554,8 @@ static int validate_cost(const leanot_cost_t* c) {
       return LEANOT_EINVAL;
     }
   } else if (c->kind == LEANOT_COST_POINTS) {
-    if (!c->feat || c->dim < 1 || c->dim > 4 || c->p < 1 || c->p > 3) {
-      set_error("points cost needs features with 1 <= dim <= 4 and p in {1,2,3}");
+    if (!c->feat || c->dim < 1 || c->dim > 4 || c->p < 1 || c->p > 3 || (reinterpret_cast<uintptr_t>(c->feat) & 15)) {
+      set_error("points cost needs 16-byte aligned features with 1 <= dim <= 4 and p in {1,2,3}");
       return LEANOT_EINVAL;
     }
   } else if (c->kind == LEANOT_COST_GRID) {

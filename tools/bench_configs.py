@@ -71,7 +71,8 @@ def config2(timeout):
     prm = dxg.params_tuned(1e-6).with_overrides(tau_mu=0.05)
     eng = DxgEngine(k, r.weights, c.weights, prm)
     eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
-    per_iter = timed_iters(eng, 50)
+    timed_iters(eng, 10)             # warm-up (lazy kernel attributes, occupancy queries)
+    per_iter = timed_iters(eng, 200)
     t0 = time.perf_counter()
     sol = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-4, timeout=None, max_iter=int(timeout / per_iter)),
                     dense_cap=0)
