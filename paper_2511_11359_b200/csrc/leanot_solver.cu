@@ -525,8 +525,22 @@ static bool fused_default();
 
 // plans whose O(n) work fits one CTA and whose sweep covers all rows (single process):
 // launch-bound regime, fused update path (reduces the column slabs itself)
+// One-CTA update (dxg_update_small) up to this n; above it the three grid-wide kernels.
+// The single CTA is FP64-bound on its two divisions and two tanh per element: measured in
+// CUDA-graph replays (tools/upd_ab.py), the grid-wide kernels win from n ~ 5000 on
+// (n = 1e4: 370 -> 360 us per iteration; n = 3000: the single CTA is 2 us faster).
+// LEANOT_SMALL_UPD_N overrides (A/B measurements).
+static int64_t small_upd_max_n() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("LEANOT_SMALL_UPD_N");
+    v = e ? atoll(e) : 4096;
+  }
+  return v;
+}
+
 static bool small_plan(const leanot_dxg_plan_t& P) {
-  return P.n <= 16384 && P.row0 == 0 && P.row1 == P.n && !use_sep(P);
+  return P.n <= small_upd_max_n() && P.row0 == 0 && P.row1 == P.n && !use_sep(P);
 }
 
 static RowPassArgs make_rowpass(const leanot_dxg_plan_t& P) {
