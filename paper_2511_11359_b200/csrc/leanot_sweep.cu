@@ -75,7 +75,8 @@ __device__ __forceinline__ void finalize_row(const RowPassArgs& A, int k, int64_
 }
 
 template <class COST, int K, int R, bool EVAL>
-__global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(const RowPassArgs A) {
+__global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(const RowPassArgs A, int64_t rb0, int64_t rb1) {
+  // this launch finalizes rows [rb0, rb1) of [A.i0, A.i1) (local indices stay relative to A.i0)
   extern __shared__ __align__(16) char smem[];
   constexpr int NV = R * K + (EVAL ? 3 * R : 0);
   __shared__ double red[RP_THREADS / 32][NV];
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
   const COST cost(A.cost);
   const int64_t n = A.cost.n;
   const int64_t nr = A.i1 - A.i0;
-  const int64_t nblk = (nr + R - 1) / R;
+  const int64_t nblk = (rb1 - rb0 + R - 1) / R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   static_assert(!(EVAL && COST::kGram), "evaluation sweeps need C itself");
   // x = mult_k * c + nb_kj: c = C_ij, mult = -a_k, nb = -b_kj; expanded form (CostGram):
@@ -95,12 +96,12 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
   for (int k = 0; k < K; ++k) mult[k] = COST::kGram ? 2.0 * A.a[k] * A.cost.inv_scale : -A.a[k];
 
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const int64_t ib = A.i0 + blk * R;
+    const int64_t ib = rb0 + blk * R;
     typename COST::Row rows[R];
     uint32_t mlo[R][K];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      int64_t i = ib + r < A.i1 ? ib + r : A.i1 - 1;
+      int64_t i = ib + r < rb1 ? ib + r : rb1 - 1;
       rows[r] = cost.row(i);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
       if (v < R * K) {
         const int r = v / K, k = v % K;
         const int64_t i = ib + r;
-        if (i < A.i1) {
+        if (i < rb1) {
           const int64_t m = A.shift[k * A.shift_kstride + (i - A.i0)];
           int64_t mu = m;
           if constexpr (COST::kGram) mu -= gram_off(A.a[k], A.cost.inv_scale, cost.norm(i));
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
       } else if (EVAL) {
         const int q = v - R * K, r = q / 3, s = q % 3;
         const int64_t i = ib + r;
-        if (i < A.i1) A.rowstat[s * nr + (i - A.i0)] = t;
+        if (i < rb1) A.rowstat[s * nr + (i - A.i0)] = t;
       }
     }
     __syncthreads();
@@ -610,6 +611,16 @@ int num_sms() {
   return g_num_sms;
 }
 
+// LEANOT_RP_TAIL=0 disables the pass-A wave-tail split (A/B measurements)
+static bool tail_split_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LEANOT_RP_TAIL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <class COST, int K, int R, bool EVAL>
 static int launch_rowpass_t(const RowPassArgs& A, cudaStream_t st) {
   auto kern = rowpass_kernel<COST, K, R, EVAL>;
@@ -624,9 +635,31 @@ static int launch_rowpass_t(const RowPassArgs& A, cudaStream_t st) {
   }
   const int64_t nr = A.i1 - A.i0;
   const int64_t nblk = (nr + R - 1) / R;
-  int grid = (int)std::min<int64_t>(nblk, (int64_t)num_sms() * occ);
+  const int64_t slots = (int64_t)num_sms() * occ;
+  int grid = (int)std::min<int64_t>(nblk, slots);
   if (grid < 1) return LEANOT_OK;
-  kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(A);
+  // Wave tail: when the last wave of R-row blocks would fill at most half the slots, the
+  // remaining rows run as a second launch of R/2-row blocks (one wave of half-length
+  // blocks instead of a half-empty full-length one).  Row sums do not depend on R (same
+  // per-thread column order, same reductions), so the split is bitwise neutral.
+  if constexpr (R % 2 == 0) {
+    const int64_t full = (nblk / slots) * slots, rem = nblk - full;
+    if (full > 0 && rem > 0 && 2 * rem <= slots && tail_split_enabled()) {
+      const int64_t rmid = A.i0 + full * R;
+      kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(A, A.i0, rmid);
+      auto kern2 = rowpass_kernel<COST, K, R / 2, EVAL>;
+      static bool attr2 = false;
+      if (!attr2) {
+        if (cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess)
+          return LEANOT_ECUDA;
+        attr2 = true;
+      }
+      const int64_t nb2 = (A.i1 - rmid + R / 2 - 1) / (R / 2);
+      kern2<<<(int)std::min<int64_t>(nb2, slots), RP_THREADS, TAB_BYTES, st>>>(A, rmid, A.i1);
+      return LEANOT_OK;
+    }
+  }
+  kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(A, A.i0, A.i1);
   return LEANOT_OK;
 }
 

@@ -276,3 +276,26 @@ def test_persistent_paths_recompute_out_of_range_rows(n):
     assert np.all(np.isfinite(d0)) and np.all(np.isfinite(b0))
     assert rel_err(d0, d1) <= 1e-11 and rel_err(b0, b1) <= 1e-11
     assert a0 == a1 and t0 == t1 == 16
+
+
+@pytest.mark.parametrize("n,p", [(1200, 2), (1201, 1), (2500, 2)])
+def test_pass_a_wave_tail_split_vs_oracle(n, p):
+    """Point costs at sizes whose last pass-A wave is split into half-height row blocks
+    (launch_rowpass_t: n = 1200 -> 296 four-row blocks + 2 two-row blocks); the step must
+    match the oracle exactly as for unsplit sizes."""
+    dxg = _dxg()
+    from paper_2511_11359_b200 import core
+    rng = np.random.default_rng(n)
+    f = rng.random((n, 2))
+    r = O.normalized_hist(rng.random(n))
+    c = O.normalized_hist(rng.random(n))
+    k = core.ColorKernel(f, p)
+    ok = O.PointCost(f, p)
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    st = dxg.DxgState(dxg.LogOddsField(rng.uniform(-1, 1, n)),
+                      dxg.TransportLogWeights(40.0, -np.abs(rng.normal(0, 20, n)), 0.0, 40))
+    nxt = dxg.dxg_step(st, k, r, c, prm)
+    onxt = O.step(O.Iterate(st.mu.delta, 40.0, st.weights.b, 0.0, 40), ok, r, c,
+                  O.params_tuned(0.0, tau_mu=0.05))
+    assert rel_err(nxt.mu.delta, onxt.delta) <= TOL_ITER
+    assert rel_err(nxt.weights.b, onxt.b) <= TOL_ITER
