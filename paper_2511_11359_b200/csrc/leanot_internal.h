@@ -47,8 +47,9 @@ int launch_rowpass(const RowPassArgs& A, int K, bool eval, cudaStream_t st);
 int launch_rowmax(const RowPassArgs& A, int K, int64_t* out, cudaStream_t st);
 int launch_colpass(const ColPassArgs& A, int K, cudaStream_t st);
 int launch_slab_reduce(const double* slab, int splits, int K, int64_t n, double* col, cudaStream_t st);
+// vmin (optional, scale < 0, sgn = 1): per-row min_j (C_ij + v_j) from pass A -> exact shift, one read
 int launch_rowlse(const CostView& cv, int64_t i0, int64_t i1, const double* v, double sgn, double scale, double* L,
-                  cudaStream_t st);
+                  cudaStream_t st, const double* vmin = nullptr);
 int launch_rowmin(const CostView& cv, int64_t i0, int64_t i1, const double* v, double* out, cudaStream_t st);
 int launch_cost_block(const CostView& cv, int64_t i0, int64_t i1, double* out, int64_t ldo, cudaStream_t st);
 

@@ -943,9 +943,10 @@ int leanot_dxg_eval(const leanot_dxg_plan_t* P, void* stream) {
   const int64_t nr = P->row1 - P->row0;
   const double* v = P->rowstat + 2 * nr;  // row minima (eta = 0 form)
   if (P->prm.eta > 0) {
-    // LSE_j(-(C_ij + sd_j)/eta) with an exact max (dxg.py:337); the result replaces the minima
+    // LSE_j(-(C_ij + sd_j)/eta) with an exact max (dxg.py:337); the shift is -min_j(C_ij + sd_j)/eta
+    // from the evaluation sweep's row minima (one read of C), the result replaces the minima
     double* L = P->rowstat + 2 * nr;
-    LEANOT_TRY(launch_rowlse(make_view(P->cost), P->row0, P->row1, P->sd, 1.0, -1.0 / P->prm.eta, L, st));
+    LEANOT_TRY(launch_rowlse(make_view(P->cost), P->row0, P->row1, P->sd, 1.0, -1.0 / P->prm.eta, L, st, L));
     v = L;
   }
   rowstats_reduce_kernel<<<1, 1024, 0, st>>>(nr, P->row0, P->r, P->S, P->m, P->rowstat, v, P->evalbuf);

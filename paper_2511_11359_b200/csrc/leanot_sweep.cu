@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(256) slab_reduce_kernel(const double* __restri
 // two reads of the row (max, then shifted sum); evaluation-only.
 template <class COST>
 __global__ void __launch_bounds__(RP_THREADS) rowlse_kernel(const CostView cv, int64_t i0, int64_t i1, const double* v,
-                                                           double sgn, double scale, double* L) {
+                                                           double sgn, double scale, const double* vmin, double* L) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double red[RP_THREADS / 32];
   __shared__ double bc;
@@ -493,22 +493,29 @@ __global__ void __launch_bounds__(RP_THREADS) rowlse_kernel(const CostView cv, i
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
     const typename COST::Row row = cost.row(i);
-    double mx = -INFINITY;
-    for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) mx = fmax(mx, (sgn * cost.eval1(row, j) + __ldg(v + j)) * scale);
-    mx = warp_max(mx);
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = red[0];
-      for (int w = 1; w < RP_THREADS / 32; ++w) t = fmax(t, red[w]);
-      bc = t;
+    double xm;
+    if (vmin) {
+      // max_j fl(x_j * scale) = fl(min_j x_j * scale) for scale < 0 (rounding is monotone),
+      // so pass A's row minimum gives the exact max without a first read of the row
+      xm = vmin[i - i0] * scale;
+    } else {
+      double mx = -INFINITY;
+      for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) mx = fmax(mx, (sgn * cost.eval1(row, j) + __ldg(v + j)) * scale);
+      mx = warp_max(mx);
+      if (lane == 0) red[warp] = mx;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = red[0];
+        for (int w = 1; w < RP_THREADS / 32; ++w) t = fmax(t, red[w]);
+        bc = t;
+      }
+      __syncthreads();
+      xm = bc;
     }
-    __syncthreads();
-    const double xm = bc;
     double s = 0.0;
     for (int64_t j = threadIdx.x; j < n; j += RP_THREADS) {
       double y = (sgn * cost.eval1(row, j) + __ldg(v + j)) * scale - xm;
-      texp_acc(tb, fmax(y, -1000.0), 0u, s);
+      texp_acc(tb, fmin(fmax(y, -1000.0), 0.0), 0u, s);  // y <= 0 whenever xm is the exact max
     }
     s = warp_sum(s);
     __syncthreads();
@@ -811,6 +818,7 @@ struct RowLseFn {
   int64_t i0, i1;
   const double* v;
   double sgn, scale;
+  const double* vmin;
   double* L;
   cudaStream_t st;
   template <class COST>
@@ -823,14 +831,14 @@ struct RowLseFn {
     }
     int grid = (int)std::min<int64_t>(i1 - i0, (int64_t)num_sms() * 3);
     if (grid < 1) return LEANOT_OK;
-    kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(cv, i0, i1, v, sgn, scale, L);
+    kern<<<grid, RP_THREADS, TAB_BYTES, st>>>(cv, i0, i1, v, sgn, scale, vmin, L);
     return LEANOT_OK;
   }
 };
 
 int launch_rowlse(const CostView& cv, int64_t i0, int64_t i1, const double* v, double sgn, double scale, double* L,
-                  cudaStream_t st) {
-  RowLseFn f{cv, i0, i1, v, sgn, scale, L, st};
+                  cudaStream_t st, const double* vmin) {
+  RowLseFn f{cv, i0, i1, v, sgn, scale, vmin, L, st};
   return LEANOT_DISPATCH_COST(cv, f);
 }
 
