@@ -224,9 +224,10 @@ int leanot_bary_eval(const leanot_bary_plan_t* P, void* stream) {
                                                P->evalbuf + k * 4);
     colstats_reduce_kernel<<<1, 1024, 0, st>>>(n, P->col + (int64_t)k * 2 * n, P->c + k * P->ns,
                                                P->delta + k * P->ns, P->evalbuf + 64 + k * 2);
-    // log_z[k][i] = LSE_j(-(C_ij + 2 sup d_kj)/eta) (barycenter.py:186-191) into L (free after the sweep)
+    // log_z[k][i] = LSE_j(-(C_ij + 2 sup d_kj)/eta) (barycenter.py:186-191) into L (free after the sweep);
+    // exact shift from the evaluation sweep's row minima min_j(C_ij + sd_kj) (one read of C)
     LEANOT_TRY(launch_rowlse(make_view(P->cost), P->row0, P->row1, P->sd + k * P->ns, 1.0, -1.0 / P->prm.eta,
-                             P->L + (int64_t)k * nr, st));
+                             P->L + (int64_t)k * nr, st, P->rowstat + (int64_t)k * 3 * nr + 2 * nr));
   }
   // LSE over this plan's rows (all rows single-process; a shard's rows otherwise, combined by the caller)
   bary_dual_reduce_kernel<<<1, 1024, 0, st>>>(P->L, P->w, m, nr, P->evalbuf + 127);
