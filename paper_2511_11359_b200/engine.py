@@ -131,6 +131,7 @@ class DxgEngine:
             setattr(p, name, getattr(self, name).data_ptr())
         p.beta = self.beta.data_ptr() if self.beta is not None else None
         self._graphs = {}
+        self._h_in = self._h_out = None
         pos = rw > 0
         self.h_r = float(-(rw[pos] * np.log(rw[pos])).sum())  # H(r) (dxg.py:308-309, 340-341)
 
@@ -145,16 +146,39 @@ class DxgEngine:
         solve(); keep_shift: the state this engine produced last (warm row shifts);
         otherwise row maxima are computed (injected state)."""
         torch = _torch()
-        self.delta.copy_(torch.as_tensor(np.asarray(delta, dtype=float)), non_blocking=True)
-        self.b.copy_(torch.as_tensor(np.asarray(b, dtype=float)), non_blocking=True)
+        n = self.delta.numel()
+        if self._h_in is None:   # pinned staging: true async H2D, no pageable bounce
+            self._h_in = torch.empty(2 * n, dtype=torch.float64, pin_memory=True)
+            self._h_out = torch.empty(2 * n + 4, dtype=torch.float64, pin_memory=True)
+            self._h_in_done = torch.cuda.Event()
+        else:
+            self._h_in_done.synchronize()   # the previous upload has left the staging buffer
+        hv = self._h_in.numpy()
+        hv[:n] = np.asarray(delta, dtype=float)
+        hv[n:] = np.asarray(b, dtype=float)
+        with torch.cuda.device(self.device):
+            self.delta.copy_(self._h_in[:n], non_blocking=True)
+            self.b.copy_(self._h_in[n:], non_blocking=True)
+            self._h_in_done.record()
         mode = 1 if fresh else (2 if keep_shift else 0)
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_prepare(C.byref(self.plan), float(a), float(s), float(t),
                                                      mode, _lib.stream_handle()), "dxg_prepare")
 
     def read_state(self):
-        sc = self.scal[:4].cpu().tolist()
-        return self.delta.cpu().numpy(), self.b.cpu().numpy(), sc[0], sc[2], int(round(sc[3]))
+        torch = _torch()
+        if self._h_out is None:
+            sc = self.scal[:4].cpu().tolist()
+            return self.delta.cpu().numpy(), self.b.cpu().numpy(), sc[0], sc[2], int(round(sc[3]))
+        n = self.delta.numel()
+        with torch.cuda.device(self.device):   # one sync for delta, b and the scalars
+            self._h_out[:n].copy_(self.delta, non_blocking=True)
+            self._h_out[n:2 * n].copy_(self.b, non_blocking=True)
+            self._h_out[2 * n:].copy_(self.scal[:4], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        ho = self._h_out.numpy()
+        sc = ho[2 * n:].tolist()
+        return ho[:n].copy(), ho[n:2 * n].copy(), sc[0], sc[2], int(round(sc[3]))
 
     def scalars(self):
         return self.scal[:4].cpu().tolist()
