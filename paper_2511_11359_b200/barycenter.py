@@ -154,16 +154,40 @@ class BaryEngine:
             setattr(p, name, getattr(self, name).data_ptr())
         self.M = M
         self.wv = wv
+        self._h_in = self._h_out = None
 
     def _call(self, name, *args):
         with _torch().cuda.device(self.device):
             _lib.check(getattr(_lib.lib(), name)(C.byref(self.plan), *args, _lib.stream_handle()), name)
 
+    def _staging(self):
+        """Pinned host buffers (deltas | bs, and + 4 scalars on the way out) and their device
+        mirror: one async H2D per load, one synchronisation per read."""
+        torch = _torch()
+        if self._h_in is None:
+            k = 2 * self.m * self.n
+            self._h_in = torch.empty(k, dtype=torch.float64, pin_memory=True)
+            self._h_out = torch.empty(k + 4, dtype=torch.float64, pin_memory=True)
+            self._d_stage = torch.empty(k + 4, dtype=torch.float64, device=self.device)
+            self._h_in_done = torch.cuda.Event()
+        return self._h_in, self._h_out, self._d_stage
+
     def load_state(self, deltas, bs, a, s, t, fresh=False):
         torch = _torch()
         m, n, ns = self.m, self.n, self.ns
-        self.delta.view(m, ns)[:, :n].copy_(torch.as_tensor(np.ascontiguousarray(deltas, dtype=float)))
-        self.b.view(m, ns)[:, :n].copy_(torch.as_tensor(np.ascontiguousarray(bs, dtype=float)))
+        first = self._h_in is None
+        h_in, _, d = self._staging()
+        if not first:
+            self._h_in_done.synchronize()   # the previous upload has left the staging buffer
+        hv = h_in.numpy().reshape(2, m, n)
+        hv[0] = np.asarray(deltas, dtype=float).reshape(m, n)
+        hv[1] = np.asarray(bs, dtype=float).reshape(m, n)
+        with torch.cuda.device(self.device):
+            d[: 2 * m * n].copy_(h_in, non_blocking=True)
+            self._h_in_done.record()
+            dv = d[: 2 * m * n].view(2, m, n)
+            self.delta.view(m, ns)[:, :n].copy_(dv[0])
+            self.b.view(m, ns)[:, :n].copy_(dv[1])
         self._call("leanot_bary_prepare", float(a), float(s), float(t), 1 if fresh else 0)
 
     def sweep(self, evaluate=False):
@@ -197,10 +221,20 @@ class BaryEngine:
         self._call("leanot_bary_update")
 
     def read_state(self):
-        sc = self.scal[:4].cpu().tolist()
+        torch = _torch()
         m, n, ns = self.m, self.n, self.ns
-        return (self.delta.view(m, ns)[:, :n].cpu().numpy(), self.b.view(m, ns)[:, :n].cpu().numpy(), sc[0], sc[2],
-                int(round(sc[3])))
+        _, h_out, d = self._staging()
+        k = 2 * m * n
+        with torch.cuda.device(self.device):
+            dv = d[:k].view(2, m, n)
+            dv[0].copy_(self.delta.view(m, ns)[:, :n])
+            dv[1].copy_(self.b.view(m, ns)[:, :n])
+            d[k:].copy_(self.scal[:4])
+            h_out.copy_(d, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        ho = h_out.numpy()
+        sc = ho[k:].tolist()
+        return ho[: m * n].reshape(m, n).copy(), ho[m * n: k].reshape(m, n).copy(), sc[0], sc[2], int(round(sc[3]))
 
     def barycenter(self):
         """r_now of the last sweep = barycenter_marginal(state) (barycenter.py:100-105)."""
