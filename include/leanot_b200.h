@@ -103,7 +103,7 @@ typedef struct leanot_dxg_plan {
   double* col;          /* 2*n  reduced column marginals (col_now | col_bar) */
   double* partial;      /* 2*nblk_upd block maxima */
   double* evalbuf;      /* 16 evaluation scalars */
-  int32_t* flags;       /* 2 + 2*nr fixup list (count, -, entries) */
+  int32_t* flags;       /* 2 + 4*nr int32: fixup list [count, -, (k, li) pairs]; up to 2 weight sets x nr rows */
   double* beta;         /* 2*((n+1)&~1) scratch for expanded-form sweeps (cost.norms set); may be null */
 } leanot_dxg_plan_t;
 
@@ -111,15 +111,16 @@ typedef struct leanot_dxg_plan {
 int leanot_version(void);
 const char* leanot_last_error(void);
 int leanot_device_sm_count(int device, int* out);
-/* bytes of workspace the sweeps need for given sizes (informational) */
+/* column-pass row splits the engine sizes plan.slab with (splits*2*n doubles) for n columns, `rows` rows */
 int leanot_dxg_default_splits(int64_t n, int64_t rows, int* out);
 
 /* ---- cost kernels (core.py:167-288) ----------------------------------- */
 /* rows [i0,i1) of the normalized cost into out (row-major, stride ldo): CostKernel.block */
 int leanot_cost_block(const leanot_cost_t* cost, int64_t i0, int64_t i1, double* out, int64_t ldo, void* stream);
-/* out[0] = max over all entries of the raw matrix (ExplicitKernel scale, core.py:255) */
+/* out[0] = max and out[1] = -min over all entries of the raw matrix (ExplicitKernel scale and the
+   negative-entry check, core.py:252-258); scratch holds 2048 doubles */
 int leanot_stored_max(const double* mat, int64_t rows, int64_t cols, int64_t ld, double* out, double* scratch, void* stream);
-/* mat /= scale (in place, IEEE division as core.py:258); also reports min via out_min (negativity check) */
+/* mat /= scale (in place, IEEE division as core.py:258) */
 int leanot_stored_normalize(double* mat, int64_t rows, int64_t cols, int64_t ld, double scale, void* stream);
 /* raw sup over all pairs of ||f_i - f_j||_p^p (ColorKernel scale, core.py:279-284) */
 int leanot_points_sup(const double* feat, int64_t n, int dim, int p, double* out, double* scratch, void* stream);
