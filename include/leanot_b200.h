@@ -162,7 +162,16 @@ int leanot_dxg_prepare(const leanot_dxg_plan_t* plan, double a, double s, double
 /* stored cost, plain iteration: one persistent launch, pass B re-reads C from L2
  * (csrc/leanot_fused.cu; experimental, slower than the two-pass kernels as of r01) */
 #define LEANOT_SWEEP_FUSED 8
+/* stored cost, plain iteration, n >= 32768 and n <= 704 x #SMs: the single-read, single-exp
+ * sweep (csrc/leanot_sr.cu) is the DEFAULT; TWO_PASS forces passes A + B instead, SINGLE_READ
+ * forces the single-read sweep below its n threshold (tests) */
+#define LEANOT_SWEEP_TWO_PASS 16
+#define LEANOT_SWEEP_SINGLE_READ 32
 int leanot_dxg_sweep(const leanot_dxg_plan_t* plan, int flags, void* stream);
+/* debug: device buffer of 2 x 8 x 4096 uint64 that later single-read sweeps (<= 4096 panels)
+ * fill with per-panel clock64 stamps of CTAs 0 and G-1 (csrc/leanot_sr.cu); null disables
+ * (the default) */
+int leanot_debug_sr_trace(void* buf);
 /* O(n) updates after plan->col holds the (globally reduced) marginals: state <- next state */
 int leanot_dxg_update(const leanot_dxg_plan_t* plan, void* stream);
 /* evaluation scalars from the last eval sweep: evalbuf[0..] = {cost_rows, ent_rows, inner_rows (eta=0 min

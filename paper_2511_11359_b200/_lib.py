@@ -90,6 +90,7 @@ def lib():
         "leanot_row_lse_affine": ([C.POINTER(CostT), i64, i64, vp, dbl, dbl, vp, vp], C.c_int),
         "leanot_dxg_prepare": ([C.POINTER(DxgPlanT), dbl, dbl, dbl, C.c_int, vp], C.c_int),
         "leanot_dxg_sweep": ([C.POINTER(DxgPlanT), C.c_int, vp], C.c_int),
+        "leanot_debug_sr_trace": ([vp], C.c_int),
         "leanot_dxg_update": ([C.POINTER(DxgPlanT), vp], C.c_int),
         "leanot_dxg_eval": ([C.POINTER(DxgPlanT), vp], C.c_int),
         "leanot_dxg_iterate": ([C.POINTER(DxgPlanT), C.c_int, vp], C.c_int),
@@ -132,7 +133,7 @@ EXPORTS = (
     "leanot_bary_rows", "leanot_bary_rnorm", "leanot_bary_cols", "leanot_dxg_iterate_eval",
     "leanot_hash_fill", "leanot_sweep_ws_doubles", "leanot_column_marginals", "leanot_row_lse",
     "leanot_plan_stats", "leanot_row_min", "leanot_row_lse_affine", "leanot_dxg_prepare",
-    "leanot_dxg_sweep", "leanot_dxg_update", "leanot_dxg_eval", "leanot_dxg_iterate",
+    "leanot_dxg_sweep", "leanot_debug_sr_trace", "leanot_dxg_update", "leanot_dxg_eval", "leanot_dxg_iterate",
     "leanot_graph_create", "leanot_graph_launch", "leanot_graph_destroy", "leanot_bary_rmap",
     "leanot_sync", "leanot_bary_prepare", "leanot_bary_sweep", "leanot_bary_update", "leanot_bary_eval",
     "leanot_col_lse_ws_doubles", "leanot_col_lse", "leanot_eta_log_minus", "leanot_sinkhorn_psi", "leanot_eot_dual",

@@ -8,3 +8,4 @@
 #include "leanot_sep.cu"
 #include "leanot_persist.cu"
 #include "leanot_fused.cu"
+#include "leanot_sr.cu"

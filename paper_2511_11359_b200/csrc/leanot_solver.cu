@@ -522,6 +522,8 @@ static int try_rowowner_iterate_eval(const leanot_dxg_plan_t& P, int iters, int 
 // single-launch L2-reuse sweep for stored costs (leanot_fused.cu)
 static int try_fused_sweep(const leanot_dxg_plan_t& P, cudaStream_t st);
 static bool fused_default();
+// single-read, single-exp sweep for stored costs (leanot_sr.cu)
+static int try_sr_sweep(const leanot_dxg_plan_t& P, cudaStream_t st, bool force);
 
 // plans whose O(n) work fits one CTA and whose sweep covers all rows (single process):
 // launch-bound regime, fused update path (reduces the column slabs itself)
@@ -902,6 +904,11 @@ int leanot_dxg_sweep(const leanot_dxg_plan_t* P, int flags, void* stream) {
       ((flags & LEANOT_SWEEP_FUSED) || fused_default())) {
     const int rc = try_fused_sweep(*P, st);
     if (rc == LEANOT_OK) return check_launch("dxg_sweep(fused)");
+    if (rc != LEANOT_EINVAL) return rc;
+  }
+  if (!eval && !gram && !(flags & (LEANOT_SWEEP_ROWS_ONLY | LEANOT_SWEEP_COLS_ONLY | LEANOT_SWEEP_TWO_PASS))) {
+    const int rc = try_sr_sweep(*P, st, (flags & LEANOT_SWEEP_SINGLE_READ) != 0);
+    if (rc == LEANOT_OK) return check_launch("dxg_sweep(single-read)");
     if (rc != LEANOT_EINVAL) return rc;
   }
   if (!(flags & LEANOT_SWEEP_COLS_ONLY)) LEANOT_TRY(launch_rowpass(A, 2, eval, st));

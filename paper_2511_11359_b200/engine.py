@@ -187,9 +187,16 @@ class DxgEngine:
     def _stream(self):
         return _lib.stream_handle()
 
-    def sweep(self, evaluate=False, fused=False):
-        """fused: stored costs only -- the experimental single-launch sweep (csrc/leanot_fused.cu)"""
+    def sweep(self, evaluate=False, fused=False, single_read=None):
+        """fused: stored costs only -- the experimental L2-reuse sweep (csrc/leanot_fused.cu).
+        single_read: None = library default (the single-read, single-exp sweep of
+        csrc/leanot_sr.cu for stored costs with n >= 32768), True = force it (any eligible n),
+        False = the two-pass sweep."""
         flags = (1 if evaluate else 0) | (8 if fused else 0)
+        if single_read is True:
+            flags |= 32
+        elif single_read is False:
+            flags |= 16
         with _torch().cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_sweep(C.byref(self.plan), flags, self._stream()), "dxg_sweep")
         if self.world > 1:

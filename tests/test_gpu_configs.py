@@ -1,0 +1,175 @@
+"""Reference parity at BASELINE config shapes 2 and 5 (needs a B200).
+
+Fixtures come from the REFERENCE run in the build container (oracle/gen_golden_configs.py):
+
+* config 2 (n = 1e4 2-D points, ColorKernel p = 2, params_tuned(1e-6) + tau_mu = 0.05) at
+  its FULL size: 50 reference iterations (dxg.py:261-279) with evaluations at 25 and 50
+  (dxg.py:412-417).  The GPU runs the default n > 1024 path: expanded-form (Gram) sweeps,
+  the eta > 0 evaluation whose exact row shift comes from pass A's row minima.
+  Tolerances (north_star): iterates 1e-10 relative, primal/dual 1e-8 relative.
+* config 5's instance family (Gaussian-mixture marginals on GridKernel(side, side, 2), m = 8,
+  tuned(1e-3) + tau_mu = 0.05) at the largest sides the reference runs in minutes: one
+  dxgb_step + evaluation + r-map from an injected state at side 40 and a solve to
+  eps = 1e-3 at side 16 (950 iterations).  Grid plans run the separable path (leanot_sep.cu),
+  whose tensor-core (DMMA) / log-domain switch is decided on device.
+* config 5 at its FULL size (316 x 316, m = 8): the separable sweep against the dense
+  definitions on sampled rows / columns (row log-normalizers L_ki = LSE_j -(a C_ij + b_kj)
+  and column marginals sum_i r_i exp(-(a C_ij + b_kj) - L_ki), barycenter.py:78-105), with
+  the r-map recomputed by the reference's sorted-k rule from the device's L.
+"""
+
+import numpy as np
+import pytest
+
+import leanot_oracle as O
+from helpers import load, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _config2():
+    from paper_2511_11359_b200 import core, dxg
+    d = load("config2_n1e4")
+    k = core.ColorKernel(d["features"], 2)
+    r, c = core.Histogram(d["r"]), core.Histogram(d["c"])
+    prm = dxg.params_tuned(1e-6).with_overrides(tau_mu=0.05)
+    return d, k, r, c, prm
+
+
+def test_config2_full_size_iterates_match_reference():
+    from paper_2511_11359_b200 import dxg
+    d, k, r, c, prm = _config2()
+    n = k.n
+    st = dxg.DxgState.initial(n)
+    for it in range(1, 51):
+        st = dxg.dxg_step(st, k, r, c, prm)
+        if f"delta_{it}" in d:
+            assert rel_err(st.mu.delta, d[f"delta_{it}"]) <= 1e-10, it
+            assert rel_err(st.weights.b, d[f"b_{it}"]) <= 1e-10, it
+            sc = d[f"scal_{it}"]
+            assert st.weights.a == sc[0] and st.weights.s == sc[1] and st.weights.t == int(sc[2])
+
+
+def test_config2_full_size_solve_evaluations_match_reference():
+    """solve(log_stride=25) over 50 iterations: the two logged points (eta = 1e-6 evaluation)."""
+    from paper_2511_11359_b200 import dxg
+    d, k, r, c, prm = _config2()
+    sol = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-4, max_iter=50), log_stride=25, dense_cap=0)
+    got = np.array([[p.iter, p.primal, p.dual, p.gap, p.col_infeas_l1, p.s] for p in sol.trajectory])
+    ref = d["evals"]
+    assert got.shape == ref.shape and np.array_equal(got[:, 0], ref[:, 0])
+    assert rel_err(got[:, 1], ref[:, 1]) <= 1e-8
+    assert rel_err(got[:, 2], ref[:, 2]) <= 1e-8
+    assert rel_err(got[:, 4], ref[:, 4]) <= 1e-8
+    assert np.array_equal(got[:, 5], ref[:, 5])
+    assert rel_err(sol.state.mu.delta, d["delta_50"]) <= 1e-10
+    assert rel_err(sol.state.weights.b, d["b_50"]) <= 1e-10
+
+
+def _bary40():
+    from paper_2511_11359_b200 import barycenter as B
+    from paper_2511_11359_b200 import core, dxg
+    d = load("bary_config5_shape")
+    g = core.GridKernel(40, 40, 2)
+    prm = dxg.DxgParams(*[float(v) for v in d["params"]])
+    margs = [core.Histogram(h) for h in d["margs40"]]
+    w = np.full(len(margs), 1.0 / len(margs))
+    st = B.BarycenterState(d["in_deltas"].copy(), d["in_bs"].copy(), float(d["in_scalars"][0]),
+                           float(d["in_scalars"][1]), int(d["in_scalars"][2]), w, prm.eta)
+    return B, dxg, d, g, prm, margs, w, st
+
+
+def test_config5_shape_step_evaluation_rmap_match_reference():
+    B, dxg, d, g, prm, margs, w, st = _bary40()
+    nxt = B.dxgb_step(st, g, margs, prm)
+    assert rel_err(nxt.deltas, d["out_deltas"]) <= 1e-10
+    assert rel_err(nxt.bs, d["out_bs"]) <= 1e-10
+    assert [nxt.a, nxt.s, nxt.t] == d["out_scalars"].tolist()
+    r = B.barycenter_marginal(nxt, g)
+    assert rel_err(r.weights, d["rmap"]) <= 1e-12
+    eng = B.BaryEngine(g, margs, w, prm)
+    eng.load_state(d["out_deltas"], d["out_bs"], *[float(x) for x in d["out_scalars"][:2]], int(d["out_scalars"][2]))
+    eng.sweep(evaluate=True)
+    primal, dual, infeas = eng.evaluate()
+    assert abs(primal - float(d["eval_primal"])) <= 1e-10 * max(1.0, abs(float(d["eval_primal"])))
+    assert abs(dual - float(d["eval_dual"])) <= 1e-10 * max(1.0, abs(float(d["eval_dual"])))
+    assert rel_err(np.asarray(infeas), d["eval_infeas"]) <= 1e-9
+
+
+def test_config5_shape_solve_same_iterations_as_reference():
+    from paper_2511_11359_b200 import barycenter as B
+    from paper_2511_11359_b200 import core, dxg
+    d = load("bary_config5_shape")
+    g = core.GridKernel(16, 16, 2)
+    prm = dxg.DxgParams(*[float(v) for v in d["params"]])
+    margs = [core.Histogram(h) for h in d["margs16"]]
+    w = np.full(len(margs), 1.0 / len(margs))
+    sol = B.dxgb_solve(g, margs, w, prm, dxg.Termination(eps=1e-3, max_iter=20000), log_stride=25)
+    assert sol.converged == bool(d["solve_converged"])
+    assert sol.iterations == int(d["solve_iterations"])
+    got = np.array([[p.iter, p.primal, p.dual, p.gap, p.col_infeas_l1, p.s] for p in sol.trajectory])
+    ref = d["solve_traj"]
+    assert got.shape == ref.shape and np.array_equal(got[:, 0], ref[:, 0])
+    assert rel_err(got[:, 1], ref[:, 1]) <= 1e-8 and rel_err(got[:, 2], ref[:, 2]) <= 1e-8
+    assert rel_err(sol.barycenter.weights, d["solve_bary"]) <= 1e-9
+
+
+def _config5_full():
+    """tools/bench_configs.py:config5's instance (316 x 316 Gaussian mixtures, m = 8)."""
+    from paper_2511_11359_b200 import core, dxg
+    side, m = 316, 8
+    rng = np.random.default_rng(5)
+    xs, ys = np.meshgrid(np.arange(side), np.arange(side), indexing="ij")
+    margs = []
+    for _ in range(m):
+        img = np.zeros((side, side))
+        for _ in range(rng.integers(2, 5)):
+            cx, cy = rng.uniform(0, side - 1, 2)
+            sig = rng.uniform(side / 8.0, side / 3.0)
+            img += rng.uniform(0.3, 1.0) * np.exp(-((xs - cx) ** 2 + (ys - cy) ** 2) / (2 * sig ** 2))
+        h = img.ravel() / img.sum() + 1e-6
+        margs.append(core.Histogram(h / h.sum()))
+    g = core.GridKernel(side, side, 2)
+    prm = dxg.params_tuned(1e-3).with_overrides(tau_mu=0.05)
+    return g, margs, np.full(m, 1.0 / m), prm
+
+
+def _lse(x):
+    mx = x.max()
+    return mx + np.log(np.exp(x - mx).sum())
+
+
+@pytest.mark.parametrize("a", [20.0, 400.0])
+def test_config5_full_size_separable_sweep_vs_dense_samples(a):
+    from paper_2511_11359_b200 import barycenter as B
+    g, margs, w, prm = _config5_full()
+    n, m = g.n, len(margs)
+    rng = np.random.default_rng(int(a))
+    deltas = rng.uniform(-0.5, 0.5, (m, n))
+    bs = -np.abs(rng.normal(0.0, 0.02 * a, (m, n)))
+    bs -= bs.max(axis=1, keepdims=True)
+    eng = B.BaryEngine(g, margs, w, prm)
+    eng.load_state(deltas, bs, a, 0.01, 50)
+    eng.sweep()
+    L = eng.L[: m * n].cpu().numpy().reshape(m, n)          # [w = 0][k][i]
+    rdev = eng.r[:n].cpu().numpy()
+    col = eng.col.cpu().numpy().reshape(m, 2, n)[:, 0, :]     # [k][w][j], w = 0
+    cost = O.GridCost(316, 316, 2)
+    rows = [0, 1, 315, 316, 49_927, n - 317, n - 1]
+    for i in rows:                                          # L_ki densely (barycenter.py:78-87)
+        Ci = cost.block(i, i + 1)[0]
+        for k in range(m):
+            ref = _lse(-(a * Ci + bs[k]))
+            assert abs(L[k, i] - ref) <= 1e-12 * max(1.0, abs(ref)), (i, k)
+    # r-map from the device's L by the reference's sorted-k rule (barycenter.py:90-97)
+    gsum = np.sort(w[:, None] * L, axis=0).sum(axis=0)
+    gsum -= gsum.max()
+    e = np.exp(gsum)
+    assert rel_err(rdev, e / e.sum()) <= 1e-12
+    for j in [0, 7, 316, 50_001, n - 1]:                    # C is symmetric: column j = row j
+        Cj = cost.block(j, j + 1)[0]
+        for k in range(m):
+            ref = float(np.sum(rdev * np.exp(-(a * Cj + bs[k, j]) - L[k])))
+            assert abs(col[k, j] - ref) <= 1e-11 * ref + 1e-18, (j, k)
+    for k in range(m):                                      # mass: sum_j col_kj = sum_i r_i = 1
+        assert abs(col[k].sum() - 1.0) <= 1e-12
