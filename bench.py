@@ -237,6 +237,9 @@ def time_to_eps_config1():
 def run_b200(args):
     import torch
     world, rank, local, group = init_dist(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}, or plain `bench.py --gpus N`)")
     from paper_2511_11359_b200 import core, dxg
     from paper_2511_11359_b200.engine import DxgEngine, shard_rows
 
@@ -391,9 +394,24 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks (one process per
+    GPU, NCCL) with torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
     else:
         run_b200(a)

@@ -162,9 +162,10 @@ int leanot_dxg_prepare(const leanot_dxg_plan_t* plan, double a, double s, double
 /* stored cost, plain iteration: one persistent launch, pass B re-reads C from L2
  * (csrc/leanot_fused.cu; experimental, slower than the two-pass kernels as of r01) */
 #define LEANOT_SWEEP_FUSED 8
-/* stored cost, plain iteration, n >= 32768 and n <= 704 x #SMs: the single-read, single-exp
- * sweep (csrc/leanot_sr.cu) is the DEFAULT; TWO_PASS forces passes A + B instead, SINGLE_READ
- * forces the single-read sweep below its n threshold (tests) */
+/* stored cost, plain iteration, n <= 704 x #SMs: SINGLE_READ runs the single-read, single-exp
+ * sweep (csrc/leanot_sr.cu; one read of C, one exp per element and weight set; opt-in, slower
+ * than the two-pass sweep at n = 1e5 as of r02 -- the default when LEANOT_SR=1 and n >= 32768);
+ * TWO_PASS forces passes A + B */
 #define LEANOT_SWEEP_TWO_PASS 16
 #define LEANOT_SWEEP_SINGLE_READ 32
 int leanot_dxg_sweep(const leanot_dxg_plan_t* plan, int flags, void* stream);

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from .core import CostKernel, Histogram, as_device_kernel, as_weights
-from .engine import default_group
+from .engine import any_rank, default_group
 from .dxg import (DxgParams, LogOddsField, Termination, TrajectoryPoint, TransportLogWeights, _plan_stats,
                   _to_dev, _ws, _wsets)
 
@@ -194,11 +194,10 @@ class BaryEngine:
         if not self.sharded:
             self._call("leanot_bary_sweep", 1 if evaluate else 0)
             return
-        import torch.distributed as dist
-        from .engine import combine_partials
+        from .engine import all_reduce_max, combine_partials
         self.sweep_rows(evaluate)
         if self.world > 1:
-            dist.all_reduce(self.gmax, op=dist.ReduceOp.MAX, group=self.group)   # order-independent
+            self.gmax.copy_(all_reduce_max(self.gmax, self.group))   # order-independent
         self.sweep_rnorm()
         if self.world > 1:
             self.esum.copy_(combine_partials(self.esum, self.group, self.world))
@@ -245,8 +244,8 @@ class BaryEngine:
     def _combine_eval(self):
         torch = _torch()
         import torch.distributed as dist
-        gathered = torch.empty(self.world * self.evalbuf.numel(), dtype=torch.float64, device=self.evalbuf.device)
-        dist.all_gather_into_tensor(gathered, self.evalbuf, group=self.group)
+        from .engine import all_gather_flat
+        gathered = all_gather_flat(self.evalbuf, self.group, self.world)
         bufs = gathered.view(self.world, -1).cpu().numpy()
         self.evalbuf.copy_(torch.from_numpy(_combine_eval_buffers(bufs, self.m)))
 
@@ -258,8 +257,8 @@ class BaryEngine:
         per = (self.n + self.world - 1) // self.world
         buf = torch.zeros(per, dtype=full.dtype, device=full.device)
         buf[: self.row1 - self.row0] = full[self.row0:self.row1]
-        out = torch.empty(per * self.world, dtype=full.dtype, device=full.device)
-        dist.all_gather_into_tensor(out, buf, group=self.group)
+        from .engine import all_gather_flat
+        out = all_gather_flat(buf, self.group, self.world)
         res = torch.empty_like(full)
         for q in range(self.world):
             a, b = shard_rows(self.n, self.world, q)
@@ -418,6 +417,8 @@ def dxgb_solve(kernel: CostKernel, marginals, w, params: DxgParams, termination:
         if termination.timeout is not None:
             torch.cuda.synchronize(eng.device)
             timed_out = time.perf_counter() - t0 > termination.timeout
+            if eng.world > 1:   # every rank must take the same branch (collectives below)
+                timed_out = any_rank(timed_out, eng.group)
         if it % log_stride == 0 or it == termination.max_iter or timed_out:
             eng.sweep(evaluate=True)
             swept = True

@@ -47,8 +47,7 @@ constexpr int SR_ALL = SR_THREADS + 32;      // 12 warps: 168 registers per thre
 constexpr int SR_NS = 4;                     // C ring slots (one panel each)
 constexpr int SR_NSLOT = 16;                 // partial-sum slots in flight (>= 2 D)
 constexpr int SR_CPC = 40;                   // max CTAs per collector chunk (G <= 4 x 40)
-constexpr int SR_NCB = 2;                    // collector prefetch buffers (panel q + 1 while q completes)
-constexpr int SR_CBUF = 4 * SR_CPC * 8 * 8;  // bytes per prefetched panel (G x 2P doubles, P <= 4)
+constexpr int SR_NR = 4;                     // per-warp row-sum buffers in flight (>= D + 1)
 constexpr uint64_t SR_TIMEOUT_NS = 4000000000ull;
 
 template <int P>
@@ -58,11 +57,10 @@ struct SrLayout {
   static constexpr int HDR = 64;                        // shift values of the panel (P <= 8)
   static constexpr int SLOT = HDR + P * ROWB;
   static constexpr int RING = TAB_BYTES;                // ring after the exp table
-  static constexpr int RED = RING + SR_NS * SLOT;       // [2][CW][NV] doubles
-  static constexpr int WB = RED + 2 * SR_CW * NV * 8;   // [D][NV] doubles + [D][NV + 1] ints (<= 8 D)
+  static constexpr int RED = RING + SR_NS * SLOT;       // [SR_NR][CW][NV] doubles
+  static constexpr int WB = RED + SR_NR * SR_CW * NV * 8;  // [D][NV] doubles + [D][NV + 1] ints (<= 8 D)
   static constexpr int BAR = WB + 8 * (NV * 8 + (NV + 1) * 4 + 8);  // mbarriers (up to 8 D slots)
-  static constexpr int CB = (BAR + 8 * (2 * SR_NS + 16) + 16 + 127) & ~127;  // [SR_NCB][SR_CBUF]
-  static constexpr int SMEM = CB + SR_NCB * SR_CBUF;
+  static constexpr int SMEM = BAR + 8 * (2 * SR_NS + 16) + 16;
   static_assert(P <= 4 && (32 % NV) == 0, "SR panel shape (collector buffers hold 2P <= 8 values per CTA)");
 };
 
@@ -90,20 +88,27 @@ __device__ __forceinline__ uint64_t sr_now() {
   return t;
 }
 
-// mbarrier wait that gives up after SR_TIMEOUT_NS (sets *abort; later waits return at once)
-__device__ __forceinline__ void sr_wait(uint64_t* bar, uint32_t parity, volatile int* abort) {
+// mbarrier wait that gives up after SR_TIMEOUT_NS (sets *abort; later waits return at once).
+// try_wait carries a suspend-time hint, so a waiting warp sleeps in hardware instead of
+// spinning (it would otherwise take issue slots from the warps it waits for).
+__device__ __forceinline__ bool sr_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-  if (ok) return;
-  const uint64_t t0 = sr_now();
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    if (ok || *abort) return;
-    if (sr_now() - t0 > SR_TIMEOUT_NS) { *abort = 1; return; }
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void sr_wait(uint64_t* bar, uint32_t parity, volatile int* abort) {
+  if (sr_try(bar, parity)) return;
+  uint64_t t0 = 0;
+  for (uint32_t spin = 1;; ++spin) {
+    if (sr_try(bar, parity)) return;
+    if ((spin & 255) == 0) {   // the clock and the abort flag are consulted every 256 polls
+      if (*abort) return;
+      const uint64_t t = sr_now();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > SR_TIMEOUT_NS) { *abort = 1; return; }
+    }
   }
 }
 
@@ -162,7 +167,7 @@ __device__ __forceinline__ double warp_transpose_sum(double (&x)[NV], int lane) 
   }
 }
 
-template <int P, int D>
+template <int P, int D, bool TRACE>
 __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
   using L = SrLayout<P>;
   constexpr int NV = L::NV;
@@ -175,15 +180,14 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
   uint64_t* wready = full + SR_NS;
   uint64_t* wfree = wready + D;
   volatile int* s_abort = reinterpret_cast<volatile int*>(wfree + D);
-  uint64_t* cbar = wfree + D + 1;                                   // [SR_NCB] collector prefetch
-  char* cbuf = smem + L::CB;
-  static_assert(SR_NS + 2 * D + 1 + SR_NCB <= 2 * SR_NS + 16, "SR barriers");
+  int* s_cnt = reinterpret_cast<int*>(wfree + D + 1);               // [SR_NR] warps done with a panel
+  static_assert(SR_NS + 2 * D + 1 + SR_NR / 2 <= 2 * SR_NS + 16 && SR_NR >= D + 1, "SR barriers");
   load_table(reinterpret_cast<double*>(smem));
   if (threadIdx.x == 0) {
     for (int s = 0; s < SR_NS; ++s) mbar_init(full + s, 1);
     for (int s = 0; s < D; ++s) { mbar_init(wready + s, 1); mbar_init(wfree + s, SR_CW); }
-    for (int s = 0; s < SR_NCB; ++s) mbar_init(cbar + s, 1);
     *s_abort = 0;
+    for (int i = 0; i < SR_NR; ++i) s_cnt[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -199,123 +203,129 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
   // iteration start, 2 prefetched buffer ready, 3 re-polls done, 4 g posted, 5 consumer starts
   // waiting for g, 6 consumer got g, 7 number of re-poll rounds
   unsigned long long* trace =
-      F.trace && (c == 0 || c == G - 1) ? F.trace + (c == 0 ? 0 : 8 * 4096) : nullptr;
-  if (trace && npan > 4096) trace = nullptr;
+      TRACE && F.trace && (c == 0 || c == G - 1) ? F.trace + (c == 0 ? 0 : 8 * 4096) : nullptr;
+  if (!TRACE || npan > 4096) trace = nullptr;
 
   if (threadIdx.x >= SR_COLL) {  // ------------------------- collector warp -------------------------
-    constexpr int NCH = 32 / NV;             // chunks of CTAs summed in parallel
-    const int v = lane % NV, ch = lane / NV;
-    const int cpc = (G + NCH - 1) / NCH;
-    const int cb = ch * cpc, ce = cb + cpc < G ? cb + cpc : G;
-    const int cnt = ce > cb ? ce - cb : 0;
+    // Layout of a panel's partials: [CTA c][v = 2 r + k].  Lane l loads 16-byte pairs at
+    // doubles 2 l + 64 jj: values v0 = 2 (l % 4), v0 + 1 of CTA 8 jj + l / 4, so lanes l, l ^ 4,
+    // l ^ 8, l ^ 16 hold the same two values of different CTAs and three butterfly levels
+    // finish the sums.  The order (jj ascending per lane, then the butterfly) is fixed, so
+    // every CTA computes bitwise the same S.
+    // Generation tags: a value of parity `par` carries sign bit `par`; the raw doubles are
+    // summed as they are (for par = 1 every term is negated, so S = -sum exactly) and a load
+    // is stale if any value's sign bit differs (OR of bits ^ parbits).
+    // The loads are direct relaxed loads, all in flight at once (LSU path: they do not queue
+    // behind the C-tile bulk copies in the SM's TMA unit), and software-pipelined: panel
+    // q + 1's loads are issued before panel q's S are finalized, so the L2 round trip
+    // overlaps the finalization.
+    static_assert(NV == 8, "collector layout assumes P = 4");
+    constexpr int NJ = (4 * SR_CPC * 8) / 64;              // 16-byte loads per lane covering G <= 160
+    const int cl = lane >> 2;                              // CTA offset within a group of 8
+    const int njj = (G + 7) / 8;
     bool dead = false;
-    // The panel's G x NV tagged partials (one contiguous block per slot) arrive in shared
-    // memory by cp.async.bulk; panel q + 1's copy is issued as soon as panel q's buffer has
-    // been read, so it overlaps q's re-polls (values not yet published when the copy ran:
-    // direct loads) and processing.
-    const uint32_t pbytes = (uint32_t)(G * NV * 8);
-    auto prefetch = [&](int64_t q) {
-      const int b = (int)(q % SR_NCB);
-      mbar_arrive_tx(cbar + b, pbytes);
-      bulk_g2s(cbuf + (size_t)b * SR_CBUF, F.part + (q % SR_NSLOT) * G * NV, pbytes, cbar + b);
+    double2 y[NJ];
+    auto issue = [&](int64_t q) {
+      const double2* gp = reinterpret_cast<const double2*>(F.part + (q % SR_NSLOT) * G * NV) + lane;
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj)
+        if (jj < njj && 8 * jj + cl < G) {
+          unsigned long long u0, u1;
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(u0), "=l"(u1) : "l"(gp + 32 * jj));
+          y[jj] = make_double2(__longlong_as_double((long long)u0), __longlong_as_double((long long)u1));
+        }
     };
-    if (lane == 0 && npan > 0) prefetch(0);
-    double rw_next = (lane < NV && (lane >> 1) < nr) ? __ldg(F.rw + F.i0 + (lane >> 1)) : 0.0;
+    if (npan > 0) issue(0);
+    // lanes 0..3 finalize row r = lane of each panel: r_i prefetched one panel ahead
+    double rw_next = (lane < P && lane < nr) ? __ldg(F.rw + F.i0 + lane) : 0.0;
     for (int64_t q = 0; q < npan; ++q) {
-      const int slot = (int)(q % SR_NSLOT);
-      const unsigned long long par = (unsigned long long)((q / SR_NSLOT) & 1);
-      const unsigned long long* base = F.part + ((int64_t)slot * G + cb) * NV + v;
+      const unsigned long long parbits = (unsigned long long)((q / SR_NSLOT) & 1) << 63;
       const double rw_q = rw_next;
-      if (q + 1 < npan && lane < NV) {
-        const int64_t li1 = (q + 1) * P + (lane >> 1);
+      if (q + 1 < npan && lane < P) {
+        const int64_t li1 = (q + 1) * P + lane;
         rw_next = li1 < nr ? __ldg(F.rw + F.i0 + li1) : 0.0;
       }
-      const int cbi = (int)(q % SR_NCB);
-      if (trace && lane == 0) trace[q * 8 + 1] = clock64();
-      sr_wait(cbar + cbi, (uint32_t)((q / SR_NCB) & 1), s_abort);
-      if (trace && lane == 0) trace[q * 8 + 2] = clock64();
-      const unsigned long long* sb = reinterpret_cast<const unsigned long long*>(cbuf + (size_t)cbi * SR_CBUF) +
-                                     cb * NV + v;
-      // raw[jj] keeps the tagged partial of CTA cb + jj once its generation matches
-      unsigned long long raw[SR_CPC];
-      uint64_t pending = 0;
-#pragma unroll
-      for (int jj = 0; jj < SR_CPC; ++jj) {
-        raw[jj] = jj < cnt ? sb[jj * NV] : 0ull;
-        if (jj < cnt && (raw[jj] >> 63) != par) pending |= 1ull << jj;
-      }
-      __syncwarp();
-      if (lane == 0 && q + 1 < npan) prefetch(q + 1);  // buffer (q + 1) % 2 was read at q - 1
+      if (TRACE && trace && lane == 0) trace[q * 8 + 1] = clock64();
+      double a0, a1, c0, c1;   // (v0, v1) x (even jj, odd jj)
       const uint64_t t0 = sr_now();
       int rounds = 0;
-      while (!dead && __any_sync(0xffffffffu, pending != 0)) {
+      while (true) {
+        a0 = a1 = c0 = c1 = 0.0;
+        unsigned long long bad = 0;
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+          if (jj < njj && 8 * jj + cl < G) {
+            bad |= ((unsigned long long)__double_as_longlong(y[jj].x) ^ parbits) |
+                   ((unsigned long long)__double_as_longlong(y[jj].y) ^ parbits);
+            if (jj & 1) { c0 += y[jj].x; c1 += y[jj].y; } else { a0 += y[jj].x; a1 += y[jj].y; }
+          }
+        if (!__any_sync(0xffffffffu, bad >> 63) || dead) break;
+        // some CTA had not published panel q when the loads ran: poll again
         ++rounds;
-        // all loads in flight before any is inspected: one L2 round trip per poll
-#pragma unroll
-        for (int jj = 0; jj < SR_CPC; ++jj)
-          if ((pending >> jj) & 1ull) raw[jj] = ld_relaxed_u64(base + (int64_t)jj * NV);
-#pragma unroll
-        for (int jj = 0; jj < SR_CPC; ++jj)
-          if (((pending >> jj) & 1ull) && (raw[jj] >> 63) == par) pending &= ~(1ull << jj);
-        // co-residency / protocol failure (never expected): report and drain the launch.  The
-        // global error flag (another CTA gave up) is consulted only after 1 ms of polling.
         const uint64_t el = sr_now() - t0;
         if (__any_sync(0xffffffffu, el > SR_TIMEOUT_NS || (el > 1000000ull && *(volatile int32_t*)F.err != 0))) {
-          dead = true;
+          dead = true;   // co-residency / protocol failure (never expected): report and drain
           if (lane == 0) atomicExch(F.err, 1);
+          break;
         }
+        issue(q);
       }
-      // fixed-order sum over the chunk: 4 interleaved accumulators (short dependency chains)
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (q + 1 < npan) issue(q + 1);   // next panel's round trip overlaps this finalization
+      if (TRACE && trace && lane == 0) { trace[q * 8 + 2] = clock64(); trace[q * 8 + 7] = rounds; }
+      double s0 = a0 + c0, s1 = a1 + c1;
 #pragma unroll
-      for (int jj = 0; jj < SR_CPC; ++jj)
-        if (jj < cnt && !((pending >> jj) & 1ull))
-          s4[jj & 3] += __longlong_as_double((long long)(raw[jj] & 0x7fffffffffffffffull));
-      const double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-      if (trace && lane == 0) { trace[q * 8 + 3] = clock64(); trace[q * 8 + 7] = rounds; }
-      // chunk sums in chunk order (lanes v, v + NV, v + 2 NV, ...)
-      double S = s;
-#pragma unroll
-      for (int h = 1; h < NCH; ++h) {
-        const double o = __shfl_sync(0xffffffffu, s, (v + h * NV) & 31);
-        if (ch == 0) S += o;
+      for (int o = 4; o < 32; o <<= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       }
-      const int r = v >> 1, k = v & 1;
-      const int64_t li = q * P + r;
-      const bool valid = li < nr;
-      const bool ok = valid && sum_ok(S) && !dead;
+      if (parbits) { s0 = -s0; s1 = -s1; }
+      if (TRACE && trace && lane == 0) trace[q * 8 + 3] = clock64();
+      // lanes 0..3: row r = lane, S0 = S of the current weights, S1 = S of the midpoint weights
+      const int64_t li = q * P + lane;
+      const bool valid = lane < P && li < nr;
+      const bool ok0 = valid && sum_ok(s0) && !dead, ok1 = valid && sum_ok(s1) && !dead;
+      // g = r_i / S: one correctly rounded reciprocal and a multiply (<= 1.5 ulp of the quotient)
+      const double w0 = ok0 ? rw_q * __drcp_rn(s0) : 0.0, w1 = ok1 ? rw_q * __drcp_rn(s1) : 0.0;
       const int ds = (int)(q % D);
       if (q >= D) sr_wait(wfree + ds, (uint32_t)(((q / D) - 1) & 1), s_abort);
-      if (ch == 0) {
-        wbuf[ds * NV + v] = ok ? rw_q / S : 0.0;
-        okbuf[ds * (NV + 1) + v] = ok ? 1 : 0;
+      if (lane < P) {
+        wbuf[ds * NV + 2 * lane] = w0;
+        wbuf[ds * NV + 2 * lane + 1] = w1;
+        okbuf[ds * (NV + 1) + 2 * lane] = ok0 ? 1 : 0;
+        okbuf[ds * (NV + 1) + 2 * lane + 1] = ok1 ? 1 : 0;
       }
-      const bool all = __all_sync(0xffffffffu, ch != 0 || ok);
+      const bool all = __all_sync(0xffffffffu, lane >= P || (ok0 && ok1));
       if (lane == 0) okbuf[ds * (NV + 1) + NV] = all ? 1 : 0;
-      const bool fin = ch == 0 && valid && (int)(q % G) == c;  // this CTA finalizes the panel's rows
-      int64_t m = 0;
-      if (fin) {
-        m = F.shift[li];
-        F.S[k * nr + li] = S;
-        F.m_used[k * nr + li] = m;
-        if (!ok) {
-          const int slot2 = atomicAdd(F.flags, 1);
-          F.flags[2 + 2 * slot2] = k;
-          F.flags[3 + 2 * slot2] = (int)li;
-        }
-      }
-      __syncwarp();  // both sets' lanes have read the row's shift before it is replaced
-      if (fin && ok && k == 1) F.shift[li] = m + llrint(log(S) * (1.0 / LSTEP));
       __syncwarp();
-      if (trace && lane == 0) trace[q * 8 + 4] = clock64();
+      if (TRACE && trace && lane == 0) trace[q * 8 + 4] = clock64();
       if (lane == 0) mbar_arrive(wready + ds);
+      if (valid && (int)(q % G) == c) {  // this CTA finalizes the panel's rows (off the consumers' path)
+        const int64_t m = F.shift[li];
+        F.S[li] = s0;
+        F.S[nr + li] = s1;
+        F.m_used[li] = m;
+        F.m_used[nr + li] = m;
+        if (!ok0 || !ok1) {
+          const int nf = (ok0 ? 0 : 1) + (ok1 ? 0 : 1);
+          int slot2 = atomicAdd(F.flags, nf);
+          if (!ok0) { F.flags[2 + 2 * slot2] = 0; F.flags[3 + 2 * slot2] = (int)li; ++slot2; }
+          if (!ok1) { F.flags[2 + 2 * slot2] = 1; F.flags[3 + 2 * slot2] = (int)li; }
+        }
+        if (ok1) F.shift[li] = m + llrint(log(s1) * (1.0 / LSTEP));
+      }
+      __syncwarp();
     }
     return;
   }
   // ------------------------------ consumers ------------------------------
   const uint32_t tb = lane_tab_addr(smem);
   const int warp = threadIdx.x >> 5;
-  const int64_t jt = 2 * threadIdx.x;           // local column pair
+  // Column group of this warp.  Warp w issues on SMSP w % 4; the collector (warp 11) shares
+  // SMSP 3 with warps 3 and 7, so warp 7 takes the LAST column group, which is only partly
+  // filled when W < 704 (n = 1e5: 36 of 64 columns), leaving the collector issue slots.
+  const int cgrp = warp == 7 ? SR_CW - 1 : (warp == SR_CW - 1 ? 7 : warp);
+  const int tcol = cgrp * 32 + lane;
+  const int64_t jt = 2 * tcol;                  // local column pair
   const bool has = j0 + jt < j1;                // n and W even: pairs are whole
   double na[2], nb[2][2], acc[2][2];
 #pragma unroll
@@ -328,7 +338,7 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
   double e[D][P][2][2];
   uint32_t s = 0, ph = 0;
   // thread 0: fill ring slot `slot` with panel p (row shifts + the C tile rows)
-  auto refill = [&](int64_t p, int slot) {
+  auto refill = [&](int p, int slot) {
     const int64_t li0 = p * P;
     const int rows = (int)(nr - li0 < P ? nr - li0 : P);
     char* dst = ring + slot * L::SLOT;
@@ -352,7 +362,12 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
   };
   if (threadIdx.x == 0)
     for (int q = 0; q < SR_NS && q < npan; ++q) refill(q, q);
-  auto compute = [&](int64_t p, double (&E)[P][2][2]) {
+  // running panel bookkeeping (32-bit, no divisions in the loop): reduction buffer pr = p % NR,
+  // partial-sum slot ps = p % NSLOT with generation parity pp
+  int pr = 0, ps = 0;
+  unsigned long long pp = 0;
+  const int npan32 = (int)npan;
+  auto compute = [&](int p, double (&E)[P][2][2]) {
     sr_wait(full + s, ph, s_abort);
     const char* st = ring + s * L::SLOT;
     double rs[NV];
@@ -361,7 +376,7 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
 #pragma unroll
       for (int r = 0; r < P; ++r) {
         const uint32_t ml = hdr[2 * r];
-        const double2 cc = *reinterpret_cast<const double2*>(st + L::HDR + r * L::ROWB + 16 * threadIdx.x);
+        const double2 cc = *reinterpret_cast<const double2*>(st + L::HDR + r * L::ROWB + 16 * tcol);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           E[r][k][0] = texp(tb, fma(na[k], cc.x, nb[k][0]), ml);
@@ -377,28 +392,44 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
     }
     const int used = (int)s;
     if (++s == SR_NS) { s = 0; ph ^= 1; }
+    // Row sums of the panel: warp transpose-reduce, then the LAST warp to finish the panel
+    // (smem counter) adds the CTA's warps in fixed order, publishes the CTA partials and
+    // refills the ring slot every warp has now read -- no CTA-wide barrier, so warps drift
+    // apart and one warp's reduction latency overlaps the others' exps.
     const double y = warp_transpose_sum<NV>(rs, lane);
-    double* rb = red + (p & 1) * (SR_CW * NV);
+    double* rb = red + pr * (SR_CW * NV);
     if ((lane & (32 / NV - 1)) == 0) rb[warp * NV + lane / (32 / NV)] = y;
-    asm volatile("bar.sync 1, %0;" ::"n"(SR_THREADS) : "memory");
-    // every consumer warp is past its reads of slot `used`: refill it NS panels ahead
-    if (threadIdx.x == 0 && p + SR_NS < npan) refill(p + SR_NS, used);
-    if (threadIdx.x < NV) {
-      double t = rb[threadIdx.x];
-#pragma unroll
-      for (int w = 1; w < SR_CW; ++w) t += rb[w * NV + threadIdx.x];
-      const int slot = (int)(p % SR_NSLOT);
-      const unsigned long long par = (unsigned long long)((p / SR_NSLOT) & 1);
-      const unsigned long long bits = ((unsigned long long)__double_as_longlong(t) & 0x7fffffffffffffffull) | (par << 63);
-      st_relaxed_u64(F.part + ((int64_t)slot * G + c) * NV + threadIdx.x, bits);
-      if (trace && threadIdx.x == 0) trace[p * 8] = clock64();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(s_cnt + pr, 1) == SR_CW - 1;
     }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      if (lane == 0) {
+        s_cnt[pr] = 0;   // reused NR panels later, after this CTA's partial of p + 1 is out
+        if (p + SR_NS < npan32) refill(p + SR_NS, used);
+      }
+      if (lane < NV) {
+        const volatile double* vb = rb;
+        double t = vb[lane];
+#pragma unroll
+        for (int w = 1; w < SR_CW; ++w) t += vb[w * NV + lane];
+        const unsigned long long bits = ((unsigned long long)__double_as_longlong(t) & 0x7fffffffffffffffull) | pp;
+        st_relaxed_u64(F.part + (ps * G + c) * NV + lane, bits);
+        if (TRACE && trace && lane == 0) trace[p * 8] = clock64();
+      }
+    }
+    if (++pr == SR_NR) pr = 0;
+    if (++ps == SR_NSLOT) { ps = 0; pp ^= 1ull << 63; }
   };
-  auto accumulate = [&](int64_t q, const double (&E)[P][2][2]) {
-    const int ds = (int)(q % D);
-    if (trace && threadIdx.x == 0) trace[q * 8 + 5] = clock64();
-    sr_wait(wready + ds, (uint32_t)((q / D) & 1), s_abort);
-    if (trace && threadIdx.x == 0) trace[q * 8 + 6] = clock64();
+  // fold panel q (exps E, slot ds = q % D, wready parity wpar) into the column sums
+  auto accumulate = [&](int q, const double (&E)[P][2][2], int ds, uint32_t wpar) {
+    if (TRACE && trace && threadIdx.x == 0) trace[q * 8 + 5] = clock64();
+    sr_wait(wready + ds, wpar, s_abort);
+    if (TRACE && trace && threadIdx.x == 0) trace[q * 8 + 6] = clock64();
     const double* wq = wbuf + ds * NV;
     const int* oq = okbuf + ds * (NV + 1);
     if (oq[NV]) {
@@ -423,13 +454,17 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
     }
     release(wfree + ds);
   };
-  for (int64_t p0 = 0; p0 < npan + D - 1; p0 += D) {
+  // p0 steps by D, so panel p = p0 + u keeps its exps in e[u] and panel q = p - (D - 1) is in
+  // e[(u + 1) % D] with wready slot (u + 1) % D; its use index q / D is p0 / D for u = D - 1
+  // and p0 / D - 1 otherwise (phase bit wph tracks p0 / D)
+  uint32_t wph = 0;
+  for (int p0 = 0; p0 < npan32 + D - 1; p0 += D, wph ^= 1) {
 #pragma unroll
     for (int u = 0; u < D; ++u) {
-      const int64_t p = p0 + u;
-      if (p < npan) compute(p, e[u]);
-      const int64_t q = p - (D - 1);
-      if (q >= 0 && q < npan) accumulate(q, e[(u + 1) % D]);
+      const int p = p0 + u;
+      if (p < npan32) compute(p, e[u]);
+      const int q = p - (D - 1);
+      if (q >= 0 && q < npan32) accumulate(q, e[(u + 1) % D], (u + 1) % D, u == D - 1 ? wph : wph ^ 1);
     }
   }
   if (has) {
@@ -449,12 +484,16 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
 #define LEANOT_SR_D 3
 #endif
 
-// LEANOT_SR=0 disables the single-read sweep (A/B measurements, falls back to two passes)
+// LEANOT_SR=1 makes the single-read sweep the default for eligible plans.  It is opt-in: at
+// n = 1e5 it measures 40.3 ms per iteration against 36.8 ms for the two-pass sweep
+// (profiles/r02_single_read.md: the 148-way exchange of row partials through L2 takes
+// ~1-1.5 us under full HBM load, more than the ~12 rows of exps the register file can hold
+// while it is in flight; engine.sweep(single_read=True) / LEANOT_SWEEP_SINGLE_READ force it)
 static bool sr_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("LEANOT_SR");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }
@@ -488,10 +527,13 @@ static int try_sr_sweep(const leanot_dxg_plan_t& P, cudaStream_t st, bool force 
   const int64_t W = (((P.n + G - 1) / G) + 1) & ~int64_t(1);
   if (W > SR_WMAX) return LEANOT_EINVAL;
   if (sr_ws_doubles(G) > (int64_t)P.splits * 2 * P.n) return LEANOT_EINVAL;
-  auto kern = sr_sweep_kernel<SP, SD>;
+  auto kern = g_sr_trace ? sr_sweep_kernel<SP, SD, true> : sr_sweep_kernel<SP, SD, false>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(sr_sweep_kernel<SP, SD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Lay::SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(sr_sweep_kernel<SP, SD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Lay::SMEM) != cudaSuccess)
       return LEANOT_EINVAL;
     if (cudaFuncSetAttribute(fused_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess)
       return LEANOT_EINVAL;

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from .core import DENSE_CAP, CostKernel, Histogram, as_device_kernel, as_weights
-from .engine import DxgEngine, default_group
+from .engine import DxgEngine, any_rank, default_group
 from .rounding import DenseCoupling, InfeasibilityReport, infeasibility, round_on_device, round_to_polytope
 from .sinkhorn import DualPotentials
 
@@ -505,6 +505,8 @@ def solve(kernel: CostKernel, r: Histogram, c: Histogram, params: DxgParams,
             it += 1
             torch.cuda.synchronize(eng.device)
             timed_out = time.perf_counter() - t0 > timeout
+            if eng.world > 1:   # every rank must take the same branch (collectives below)
+                timed_out = any_rank(timed_out, eng.group)
         if it % log_stride == 0 or it == max_iter or timed_out:
             # the evaluation sweep is also the next iteration's sweep
             eng.sweep(evaluate=True)

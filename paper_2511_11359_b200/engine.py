@@ -36,18 +36,68 @@ def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
     return min(n, rank * per), min(n, (rank + 1) * per)
 
 
+def _host_staged(group) -> bool:
+    """Non-NCCL backends (gloo: the CPU tests and multi-process runs on one GPU) exchange
+    device tensors through host memory."""
+    import torch.distributed as dist
+    return dist.get_backend(group) != "nccl"
+
+
+def all_gather_flat(t, group, world: int):
+    """all_gather_into_tensor of a flat copy of `t` (world x numel, rank order), on the
+    tensor's device; CUDA tensors are staged through the host on non-NCCL backends."""
+    torch = _torch()
+    import torch.distributed as dist
+    flat = t.contiguous().view(-1)
+    if flat.is_cuda and _host_staged(group):
+        h = flat.cpu()
+        out = torch.empty(world * h.numel(), dtype=h.dtype)
+        dist.all_gather_into_tensor(out, h, group=group)
+        return out.to(flat.device)
+    out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
+    dist.all_gather_into_tensor(out, flat, group=group)
+    return out
+
+
+def all_reduce_max(t, group):
+    """Element-wise MAX over ranks (order-independent, so exact); device tensors are staged
+    through the host on non-NCCL backends."""
+    import torch.distributed as dist
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        return h.to(t.device)
+    out = t.clone()
+    dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)
+    return out
+
+
+def any_rank(flag: bool, group) -> bool:
+    """True on every rank if `flag` is true on any rank (a MAX all-reduce of one int).
+
+    Control decisions taken from per-rank state -- the wall-clock timeout of solve() --
+    must agree across ranks, otherwise ranks issue different collectives and hang."""
+    if group is None:
+        return bool(flag)
+    torch = _torch()
+    import torch.distributed as dist
+    dev = torch.device("cpu") if _host_staged(group) else torch.device("cuda", torch.cuda.current_device())
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return bool(t.item())
+
+
 def combine_partials(local, group, world: int):
     """Sum per-rank partial vectors in rank order (all-gather, then fixed-order add).
 
     Deterministic and identical on every rank regardless of the collective's
     internal reduction order; works for any torch.distributed backend (NCCL on
-    the GPU box, gloo in the CPU tests).
+    the GPU box; gloo with host staging for device tensors, and plain CPU tensors in
+    the host-logic tests).
     """
     torch = _torch()
-    import torch.distributed as dist
     flat = local.contiguous().view(-1)
-    gathered = torch.empty(world * flat.numel(), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(gathered, flat, group=group)
+    gathered = all_gather_flat(flat, group, world)
     if gathered.is_cuda:
         # rank-order sum on the device (leanot_sum_partials)
         out = torch.empty_like(flat)

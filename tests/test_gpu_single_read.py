@@ -1,9 +1,8 @@
 """Single-read, single-exp sweep (stored cost, csrc/leanot_sr.cu) vs the two-pass sweep and the
 oracle (needs a B200).
 
-The single-read sweep is the default for plain DXG iterations of a stored cost with
-n >= 32768 (engine.sweep()); engine.sweep(single_read=True) forces it at smaller n,
-single_read=False runs passes A + B.  It reads C once and evaluates each exponential once,
+The single-read sweep is opt-in (engine.sweep(single_read=True), LEANOT_SR=1): it runs
+plain DXG iterations of a stored cost; single_read=False / the default runs passes A + B.  It reads C once and evaluates each exponential once,
 exchanging per-CTA row partial sums through tagged global slots; the result must be the
 same iteration.
 Tolerance: both forms sum the same terms in different fixed orders, so they agree to a few
@@ -112,16 +111,20 @@ def test_single_read_iterations_track_two_pass():
     assert a0 == a1 and s0 == s1 and t0 == t1 == 125
 
 
-def test_single_read_is_the_default_above_threshold():
-    """engine.sweep() with no mode runs the single-read kernel for n >= 32768."""
+def test_single_read_is_opt_in():
+    """engine.sweep() with no mode runs the two-pass sweep (the single-read kernel is opt-in:
+    LEANOT_SR=1 or single_read=True); forcing it leaves its slots written."""
     import torch
     from paper_2511_11359_b200.engine import DxgEngine
     n = 32768
     k, r, c, prm, st = _setup(n, 100.0, 9)
     eng = DxgEngine(k, r, c, prm)
     eng.load_state(*st)
-    eng.slab.fill_(0.0)
+    eng.slab.fill_(-1.0)       # the two-pass sweep's column slabs overwrite the error word
     eng.sweep()
+    torch.cuda.synchronize()
+    assert not _sr_ran(eng)
+    eng.sweep(single_read=True)
     torch.cuda.synchronize()
     assert _sr_ran(eng)
 
