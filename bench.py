@@ -159,11 +159,14 @@ def cpu_reference(n, seed, steps, warmup):
     sample = Sample()
 
     def one():
-        def work(i0, i1):
-            Cb = sample.block(i0, i1)
-            return [r[i0:i1] @ O._softmax_block(a, b, Cb) for a, b in wsets]
+        # dxg_step runs column_marginal twice, each a full pass over the blocks
+        # (dxg.py:272, :276; column_marginal dxg.py:193-208), so the two weight sets are two
+        # separate passes here too (no shared block read)
         t0 = time.perf_counter()
-        O.run_blocks(work, rows, workers=cores)
+        for a, b in wsets:
+            def work(i0, i1, a=a, b=b):
+                return r[i0:i1] @ O._softmax_block(a, b, sample.block(i0, i1))
+            O.run_blocks(work, rows, workers=cores)
         return time.perf_counter() - t0
 
     for _ in range(warmup):
@@ -171,8 +174,9 @@ def cpu_reference(n, seed, steps, warmup):
     times = [one() for _ in range(steps)]
     per_iter = statistics.median(times) * (n / rows)
     return {"value": 1.0 / per_iter, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{rows} of {n} rows of C (both weight sets of one dxg_step, {cores} threads, "
-                      f"numpy {np.__version__}), median of {steps}, extrapolated x{n / rows:.1f} to one iteration",
+            "sample": f"{rows} of {n} rows of C (both column_marginal passes of one dxg_step, one 128-row "
+                      f"block per thread, {cores} threads, numpy {np.__version__}), median of {steps} steps, "
+                      f"scaled x{n / rows:.1f} to one iteration (the full iteration is ~{n / rows:.0f}x the sample)",
             "seconds_per_iter": per_iter}
 
 
@@ -292,25 +296,40 @@ def run_b200(args):
     # dominant kernel = pass B (column sums); report it and the whole sweep
     t_colk = statistics.mean(t_cols)
     fp64_per_elem = 2 * 8 + 2 * 8                  # 8 FP64 instr per element and weight set in each pass
+    it_bytes_per_s = bytes_alg / (ms_per_step / 1e3)   # one read of C per iteration
     roofline = {
-        "bound": "hbm", "kernel": "colpass_kernel<CostStored,2> (pass B, column sums of both weight sets)",
-        "achieved": bytes_alg / t_colk / 1e9, "peak": peak, "unit": "GB/s",
-        "frac": bytes_alg / t_colk / 1e9 / peak, "peak_kind": peak_kind, "traffic": None,
-        "bytes_alg_per_launch": bytes_alg,
-        "limiter": "not HBM bandwidth: each pass streams C exactly once (ncu DRAM bytes = algorithmic "
-                   "bytes) while the board sits at its 1 kW cap (sw_power_cap, SM clock ~1.6 of 1.97 GHz) "
-                   "running ~8 FP64 + 7 other instructions per exp (profiles/r01_power.md, r01_sweep_ncu.md)",
+        "bound": "hbm", "what": "one DXG iteration: 8 n^2 algorithmic bytes (one read of C, SURVEY.md §8d) "
+                                "/ ms_per_step",
+        "achieved": it_bytes_per_s / 1e9, "peak": peak, "unit": "GB/s", "frac": it_bytes_per_s / 1e9 / peak,
+        "peak_kind": peak_kind, "bytes_alg_per_iteration": bytes_alg,
+        "traffic": None, "traffic_source": None,
+        "dominant_kernel": {
+            "kernel": "colpass_kernel<CostStored,2> (pass B, column sums of both weight sets)",
+            "seconds_per_launch": t_colk, "bytes_alg_per_launch": bytes_alg,
+            "achieved_gbs": bytes_alg / t_colk / 1e9, "frac": bytes_alg / t_colk / 1e9 / peak,
+            "note": "per launch: each of the two passes reads C once, so the per-launch fraction "
+                    "counts the second read as work; the iteration fraction above does not"},
+        "limiter": "the two-pass sweep reads C twice and evaluates 4 exps per element; the board "
+                   "sits at its 1 kW cap (sw_power_cap) running ~8 FP64 + 5 other instructions per exp "
+                   "(profiles/r01_power.md); the single-read kernel (csrc/leanot_sr.cu, opt-in) is "
+                   "exchange-latency bound (profiles/r02_single_read.md)",
         "sweep": {"what": "pass A + pass B (one DXG iteration's n^2 work)", "seconds": t_sweep,
                   "hbm_frac_vs_one_read": bytes_alg / t_sweep / 1e9 / peak,
                   "fp64_instr_per_s": fp64_per_elem * n * nr / t_sweep,
-                  "fp64_frac_of_measured_dfma_peak": fp64_per_elem * n * nr / t_sweep / FP64_PEAK_DFMA},
+                  "fp64_frac_of_measured_dfma_peak": fp64_per_elem * n * nr / t_sweep / FP64_PEAK_DFMA,
+                  "fp64_peak_source": "builder microbenchmark at 1965 MHz (profiles/r01_microbench.md), "
+                                      "not MEASURED_PEAKS.json"},
         "phase_ms": {"rowpass": 1e3 * statistics.mean(t_rows), "colpass": 1e3 * t_colk,
                      "update": 1e3 * statistics.mean(t_upd)},
     }
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            roofline["traffic"] = json.loads(prof.read_text()).get("colpass_dram_bytes_per_launch")
+            tj = json.loads(prof.read_text())
+            roofline["traffic"] = tj.get("colpass_dram_bytes_per_launch")
+            roofline["traffic_source"] = ("ncu --set full capture of the same kernel (profiles/traffic.json, "
+                                          "separate run, not measured in this run): dram bytes read+write per "
+                                          "pass-B launch")
         except Exception:
             pass
 
@@ -354,19 +373,22 @@ def run_b200(args):
             line["time_to_eps"] = {"error": repr(e)}
         # the headline instance's time-to-eps takes 4.5-15 min (too long for this run): the
         # committed record of the same solver on the same instance, labelled as such
-        rec = ROOT / "profiles" / "r01_tte_config3_eps2e-4.json"
+        rec = ROOT / "profiles" / "r02_tte_config3_eps1e-4.json"
+        if not rec.exists():
+            rec = ROOT / "profiles" / "r01_tte_config3_eps2e-4.json"
         if rec.exists():
             try:
                 d = json.loads(rec.read_text())
                 tr = d["trajectory_every_25"]
                 hits = {}
-                for eps in (1e-3, 2e-4):
+                for eps in (1e-3, 2e-4, 1e-4):
                     h = [p for p in tr if abs(p[4]) <= eps / 6 and p[5] <= eps / 6]
                     if h:
                         hits[str(eps)] = {"iterations": h[0][0], "seconds": h[0][1]}
                 line["time_to_eps_n1e5_recorded"] = {
-                    "source": "profiles/r01_tte_config3_eps2e-4.json (tools/tte_config3.py, separate run, "
-                              "same kernels; not timed in this run)",
+                    "measured_in_this_run": False,
+                    "source": f"profiles/{rec.name} (tools/tte_config3.py, a separate GPU run of the same "
+                              "solver; NOT measured in this run)",
                     "instance": "BASELINE config 3 (n=1e5 stored C, tuned + tau_mu=0.05)", "eps": hits}
             except Exception as e:  # report, do not hide
                 line["time_to_eps_n1e5_recorded"] = {"error": repr(e)}

@@ -55,10 +55,10 @@ typedef struct leanot_cost {
   const double* grid_coords;  /* GRID: [row index (n) | column index (n)] as doubles */
   double inv_scale;   /* 1/scale for on-the-fly kinds */
   double sup_norm;    /* ||C||_inf after normalization: 1 or 0 */
-  const double* norms;/* POINTS, p = 2, optional: |f_j|^2 (leanot_points_norms).  When set, the
-                       * non-evaluation DXG sweeps use the expanded form
-                       * a C_ij = a inv (|f_i|^2 + |f_j|^2 - 2 f_i.f_j), whose row constant
-                       * cancels in the row softmax (dxg.py:199-202) */
+  const double* norms;/* POINTS, p = 2, optional: leanot_points_norms output (|f_j - mu|^2, then the
+                       * centered features).  When set, the non-evaluation DXG sweeps use the
+                       * expanded form a C_ij = a inv (|g_i|^2 + |g_j|^2 - 2 g_i.g_j), g = f - mu,
+                       * whose row constant cancels in the row softmax (dxg.py:199-202) */
 } leanot_cost_t;
 
 /* K weight sets {a_k, b_k}: rows softmax_j(-(a_k C_ij + b_kj)) (dxg.py:185-190).
@@ -124,7 +124,10 @@ int leanot_stored_max(const double* mat, int64_t rows, int64_t cols, int64_t ld,
 int leanot_stored_normalize(double* mat, int64_t rows, int64_t cols, int64_t ld, double scale, void* stream);
 /* raw sup over all pairs of ||f_i - f_j||_p^p (ColorKernel scale, core.py:279-284) */
 int leanot_points_sup(const double* feat, int64_t n, int dim, int p, double* out, double* scratch, void* stream);
-/* out[j] = |f_j|^2 (fma chain over the dim features): leanot_cost_t.norms of a POINTS p = 2 cost */
+/* leanot_cost_t.norms of a POINTS p = 2 cost: out = [|f_j - mu|^2 (n, padded to an even count np) |
+ * f_j - mu (n x dim, row-major) | mu (dim)], mu = the per-dimension feature mean (fixed-order
+ * reduction).  The expanded-form sweeps run on the centered features (translation-invariant cost,
+ * smaller cancellation error); out holds np + n*dim + dim doubles. */
 int leanot_points_norms(const double* feat, int64_t n, int dim, double* out, void* stream);
 /* benchmark instance: C_ij = splitmix64(seed,i,j) -> U[0,1), C[0][n-1] = 1 (oracle/leanot_oracle.py:hash_u01) */
 int leanot_hash_fill(double* mat, int64_t row0, int64_t rows, int64_t n, int64_t ld, uint64_t seed, void* stream);
@@ -176,7 +179,8 @@ int leanot_debug_sr_trace(void* buf);
 /* O(n) updates after plan->col holds the (globally reduced) marginals: state <- next state */
 int leanot_dxg_update(const leanot_dxg_plan_t* plan, void* stream);
 /* evaluation scalars from the last eval sweep: evalbuf[0..] = {cost_rows, ent_rows, inner_rows (eta=0 min
- * form), infeas, c.d}; eta > 0 additionally runs the LSE dual sweep (dxg.py:335-342). */
+ * form), infeas, c.d}; eta > 0 additionally runs the LSE dual sweep (dxg.py:335-342) into S[nr, 2nr)
+ * (the sweep's row minima in rowstat stay intact: repeated calls give the same scalars). */
 int leanot_dxg_eval(const leanot_dxg_plan_t* plan, void* stream);
 /* iters x (sweep, update) -- capturable; single process only */
 int leanot_dxg_iterate(const leanot_dxg_plan_t* plan, int iters, void* stream);

@@ -99,6 +99,12 @@ class BaryEngine:
             import torch.distributed as dist
             self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         r0, r1 = kernel.local_rows
+        if self.world > 1 and kernel.cost_struct().kind == _lib.COST_GRID and (r0, r1) == (0, n):
+            # grid costs run the separable O(n^1.5) sweeps (leanot_sep.cu; config 5: 0.54 ms per
+            # iteration on one GPU).  Sharding their rows would put an exchange between every
+            # LSE-convolution stage for no gain, so every rank runs the whole iteration
+            # (identical on all ranks: replicas, no collective per iteration)
+            self.world, self.rank = 1, 0
         if self.world > 1 and (r0, r1) == (0, n):
             from .engine import shard_rows
             r0, r1 = shard_rows(n, self.world, self.rank)
@@ -417,7 +423,7 @@ def dxgb_solve(kernel: CostKernel, marginals, w, params: DxgParams, termination:
         if termination.timeout is not None:
             torch.cuda.synchronize(eng.device)
             timed_out = time.perf_counter() - t0 > termination.timeout
-            if eng.world > 1:   # every rank must take the same branch (collectives below)
+            if eng.group is not None:   # every rank must take the same branch (collectives below)
                 timed_out = any_rank(timed_out, eng.group)
         if it % log_stride == 0 or it == termination.max_iter or timed_out:
             eng.sweep(evaluate=True)

@@ -374,7 +374,9 @@ class ColorKernel(CostKernel):
         self.sup_norm = 1.0 if raw_sup > 0 else 0.0
         self.norms_dev = None
         if self.p == 2:  # |f_j|^2 for the expanded-form sweeps (leanot_cost_t.norms)
-            self.norms_dev = torch.empty(self.n, dtype=torch.float64, device=self.device)
+            # [|f_j - mu|^2 (n, even-padded) | centered features (n x dim) | mu] (leanot_points_norms)
+            npad = (self.n + 1) & ~1
+            self.norms_dev = torch.empty(npad + self.n * self.dim + self.dim, dtype=torch.float64, device=self.device)
             with torch.cuda.device(self.device):
                 _lib.check(_lib.lib().leanot_points_norms(self.features_dev.data_ptr(), self.n, self.dim,
                                                           self.norms_dev.data_ptr(), _lib.stream_handle()),

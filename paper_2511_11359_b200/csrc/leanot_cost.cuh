@@ -46,10 +46,13 @@ struct CostStored {
 #pragma unroll
     for (int r = 0; r < R; ++r) { c[r][0] = p.v[r].x; c[r][1] = p.v[r].y; }
   }
+  // the column pass owns the column pairs (j, j + 1) and (j + kPairGap, j + kPairGap + 1): each
+  // 16-byte load of a warp then covers 512 contiguous bytes (whole sectors)
+  static constexpr int kPairGap = 512;
   struct Pre4 { double2 v0, v1; };
   __device__ __forceinline__ void pre4(const Row& row, int64_t j, Pre4& p) const {
     p.v0 = __ldcs(reinterpret_cast<const double2*>(row.p + j));
-    p.v1 = __ldcs(reinterpret_cast<const double2*>(row.p + j + 2));
+    p.v1 = __ldcs(reinterpret_cast<const double2*>(row.p + j + kPairGap));
   }
   // four consecutive columns (j % 4 == 0 not required; j even), for the column pass
   struct Col4 {};
@@ -189,7 +192,9 @@ struct CostGram {
   int64_t n;
   struct Row { double v[DIM]; };
   struct Col { double v0[DIM], v1[DIM]; };
-  __device__ explicit CostGram(const CostView& v) : f(v.feat), nrm(v.norms), inv(v.inv_scale), n(v.n) {}
+  // norms buffer: [|f_j - mu|^2 (n, padded to even) | centered features f_j - mu (n x DIM)]
+  __device__ explicit CostGram(const CostView& v)
+      : f(v.norms + ((v.n + 1) & ~int64_t(1))), nrm(v.norms), inv(v.inv_scale), n(v.n) {}
   __device__ __forceinline__ Row row(int64_t i) const {
     Row r;
 #pragma unroll

@@ -466,11 +466,42 @@ __global__ void gram_beta_kernel(int64_t n, int64_t ld, const double* scal, doub
   }
 }
 
-// |f_j|^2 for the expanded (Gram) form of squared-Euclidean costs
-__global__ void points_norms_kernel(const double* f, int64_t n, int dim, double* out) {
+// Expanded (Gram) form of squared-Euclidean costs.  |f_i - f_j|^2 does not change under a
+// translation, so the form runs on features centered at their mean mu: the cancellation in
+// N_i + N_j - 2 f_i.f_j then costs ~ulp(|f - mu|^2) instead of ulp(|f|^2) (point clouds far
+// from the origin).  One CTA computes mu per dimension in a fixed order (deterministic).
+__global__ void __launch_bounds__(1024) points_mean_kernel(const double* f, int64_t n, int dim, double* mu) {
+  __shared__ double red[32][4];
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
+    for (int d = 0; d < dim; ++d) s[d] += f[j * dim + d];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = 0; d < dim; ++d) {
+    const double v = warp_sum(s[d]);
+    if (lane == 0) red[warp][d] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < dim) {
+    double t = red[0][threadIdx.x];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t += red[w][threadIdx.x];
+    mu[threadIdx.x] = t / (double)n;
+  }
+}
+
+// out[j] = |f_j - mu|^2 (j < n), out[np + j*dim + d] = f_jd - mu_d (np = n rounded up to even)
+__global__ void points_norms_kernel(const double* f, int64_t n, int dim, const double* mu, double* out) {
+  const int64_t np = (n + 1) & ~int64_t(1);
+  double m[4];
+  for (int d = 0; d < dim; ++d) m[d] = mu[d];
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    double s = f[j * dim] * f[j * dim];
-    for (int d = 1; d < dim; ++d) s = fma(f[j * dim + d], f[j * dim + d], s);
+    const double g0 = f[j * dim] - m[0];
+    out[np + j * dim] = g0;
+    double s = g0 * g0;
+    for (int d = 1; d < dim; ++d) {
+      const double g = f[j * dim + d] - m[d];
+      out[np + j * dim + d] = g;
+      s = fma(g, g, s);
+    }
     out[j] = s;
   }
 }
@@ -684,7 +715,10 @@ int leanot_points_sup(const double* feat, int64_t n, int dim, int p, double* out
 int leanot_points_norms(const double* feat, int64_t n, int dim, double* out, void* stream) {
   LEANOT_TRY(ensure_init());
   if (!feat || !out || n < 1 || dim < 1 || dim > 4) { set_error("points_norms: bad arguments"); return LEANOT_EINVAL; }
-  points_norms_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, S_(stream)>>>(feat, n, dim, out);
+  // out = [|f_j - mu|^2 (n, padded to even) | f_j - mu (n x dim) | mu (dim)]
+  double* mu = out + ((n + 1) & ~int64_t(1)) + n * dim;
+  points_mean_kernel<<<1, 1024, 0, S_(stream)>>>(feat, n, dim, mu);
+  points_norms_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, S_(stream)>>>(feat, n, dim, mu, out);
   return check_launch("points_norms");
 }
 
@@ -951,9 +985,12 @@ int leanot_dxg_eval(const leanot_dxg_plan_t* P, void* stream) {
   const double* v = P->rowstat + 2 * nr;  // row minima (eta = 0 form)
   if (P->prm.eta > 0) {
     // LSE_j(-(C_ij + sd_j)/eta) with an exact max (dxg.py:337); the shift is -min_j(C_ij + sd_j)/eta
-    // from the evaluation sweep's row minima (one read of C), the result replaces the minima
-    double* L = P->rowstat + 2 * nr;
-    LEANOT_TRY(launch_rowlse(make_view(P->cost), P->row0, P->row1, P->sd, 1.0, -1.0 / P->prm.eta, L, st, L));
+    // from the evaluation sweep's row minima (one read of C).  The LSEs go to S[nr, 2nr) (the
+    // midpoint row sums, not read after the sweep), so the minima stay intact and a second
+    // call gives the same result.
+    double* L = P->S + nr;
+    LEANOT_TRY(launch_rowlse(make_view(P->cost), P->row0, P->row1, P->sd, 1.0, -1.0 / P->prm.eta, L, st,
+                             P->rowstat + 2 * nr));
     v = L;
   }
   rowstats_reduce_kernel<<<1, 1024, 0, st>>>(nr, P->row0, P->r, P->S, P->m, P->rowstat, v, P->evalbuf);

@@ -235,6 +235,7 @@ template <class COST>
 __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double red[32];
+  __shared__ double red3[32][2];
   __shared__ double bcast;
   const int cnt = *A.flags;
   if (cnt == 0) return;
@@ -264,15 +265,32 @@ __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
     __syncthreads();
     const int64_t m = llrint(bcast * (1.0 / LSTEP));
     const uint32_t mlo = (uint32_t)m;
-    double s = 0.0;
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) texp_acc(tb, xval(j), mlo, s);
+    // evaluation sweeps: the row's plan statistics (sum e*C, sum e*x; dxg.py:282-310) were
+    // accumulated by pass A with the rejected shift, so they are recomputed with this one
+    const bool stats = !COST::kGram && A.rowstat && k == 0;
+    double s = 0.0, u = 0.0, v = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      const double c = cost.eval1(row, j);
+      const double x = fma(mult, c, COST::kGram ? A.b[k][j] : -A.b[k][j]);
+      const double e = texp(tb, x, mlo);
+      s += e;
+      if (stats) { u = fma(e, c, u); v = fma(e, x, v); }
+    }
     s = warp_sum(s);
+    if (stats) { u = warp_sum(u); v = warp_sum(v); }
     __syncthreads();
-    if (lane == 0) red[warp] = s;
+    if (lane == 0) { red[warp] = s; red3[warp][0] = u; red3[warp][1] = v; }
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = red[0];
       for (int w = 1; w < nw; ++w) t += red[w];
+      if (stats) {
+        const int64_t nr = A.i1 - A.i0;
+        double tu = red3[0][0], tv = red3[0][1];
+        for (int w = 1; w < nw; ++w) { tu += red3[w][0]; tv += red3[w][1]; }
+        A.rowstat[li] = tu;
+        A.rowstat[nr + li] = tv;
+      }
       // finalize without re-flagging
       const int64_t nr = A.i1 - A.i0;
       A.S[k * nr + li] = t;
@@ -351,10 +369,23 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
 #pragma unroll
   for (int k = 0; k < K; ++k) mult[k] = COST::kGram ? 2.0 * A.a[k] * A.cost.inv_scale : -A.a[k];
 
+  // Columns of this thread: 4 consecutive ones (on-the-fly costs), or for the stored cost two
+  // pairs 512 apart (CostStored::kPairGap) so that every 16-byte load of a warp reads whole
+  // 32-byte sectors (4 consecutive doubles per lane would use half of each sector per load).
+  auto colv = [&](int64_t tile, int v) -> int64_t {
+    if constexpr (COST::kStored)
+      return tile * CP_TILE + 2 * threadIdx.x + (v >> 1) * COST::kPairGap + (v & 1);
+    else
+      return tile * CP_TILE + CP_V * threadIdx.x + v;
+  };
+  static_assert(!COST::kStored || 2 * COST::kPairGap == CP_TILE, "stored column pass layout");
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t tile = it % ntiles, split = it / ntiles;
-    const int64_t j = tile * CP_TILE + CP_V * threadIdx.x;
-    const int nv = (int)(n - j < 0 ? 0 : (n - j > CP_V ? CP_V : n - j));
+    const int64_t j = colv(tile, 0);
+    // columns are increasing in v: the thread's valid columns are v < nv
+    int nv = 0;
+#pragma unroll
+    for (int v = 0; v < CP_V; ++v) nv += colv(tile, v) < n ? 1 : 0;
     const bool full = nv == CP_V;
     const int64_t jl = nv > 0 ? j : 0;
     const typename COST::Col4 cl = cost.col4(jl);
@@ -362,7 +393,8 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
-      for (int v = 0; v < CP_V; ++v) nb[k][v] = v < nv ? (COST::kGram ? 1.0 : -1.0) * __ldg(A.b[k] + j + v) : 0.0;
+      for (int v = 0; v < CP_V; ++v)
+        nb[k][v] = v < nv ? (COST::kGram ? 1.0 : -1.0) * __ldg(A.b[k] + colv(tile, v)) : 0.0;
     double acc[K][CP_V];
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -430,7 +462,7 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
 #pragma unroll
           for (int v = 0; v < CP_V; ++v) {
             if (v < nv) {
-              const double cv = cost.eval1(row, j + v);
+              const double cv = cost.eval1(row, colv(tile, v));
 #pragma unroll
               for (int k = 0; k < K; ++k) {
                 const double* cf = s_coef + (q * K + k) * 4;
@@ -447,7 +479,7 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
       double* out = A.slab + (split * K + k) * n;
 #pragma unroll
       for (int v = 0; v < CP_V; ++v)
-        if (v < nv) out[j + v] = acc[k][v];
+        if (v < nv) out[colv(tile, v)] = acc[k][v];
     }
   }
 }

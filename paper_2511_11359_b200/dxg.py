@@ -244,11 +244,20 @@ def column_marginal(state: TransportLogWeights, kernel: CostKernel, r: Histogram
     return _column_marginals(kernel, as_weights(r), [(state.a, state.b)])[0]
 
 
+def _holds_all_rows(kernel) -> bool:
+    return tuple(kernel.local_rows) == (0, kernel.n)
+
+
 def _plan_on_device(state: TransportLogWeights, kernel: CostKernel, r_w):
     """D_r p as a device n x n tensor: row LSEs (sweep kernels) + one plan kernel."""
     torch = _torch()
     dev = kernel.device
     n = kernel.n
+    if not _holds_all_rows(kernel):
+        # a row-restricted stored cost (HashKernel(rows=...), one rank's shard) holds rows
+        # [r0, r1) only: the dense plan would read rows it does not have
+        r0, r1 = kernel.local_rows
+        raise ValueError(f"the dense plan needs all {n} rows of the cost; this kernel holds rows [{r0}, {r1})")
     with torch.cuda.device(dev):
         bt = _to_dev(state.b, dev)
         w, keep = _wsets(dev, [(state.a, bt)])
@@ -505,7 +514,7 @@ def solve(kernel: CostKernel, r: Histogram, c: Histogram, params: DxgParams,
             it += 1
             torch.cuda.synchronize(eng.device)
             timed_out = time.perf_counter() - t0 > timeout
-            if eng.world > 1:   # every rank must take the same branch (collectives below)
+            if eng.group is not None:   # every rank must take the same branch (collectives below)
                 timed_out = any_rank(timed_out, eng.group)
         if it % log_stride == 0 or it == max_iter or timed_out:
             # the evaluation sweep is also the next iteration's sweep
@@ -527,8 +536,9 @@ def solve(kernel: CostKernel, r: Histogram, c: Histogram, params: DxgParams,
     eng.close()
     state = DxgState(LogOddsField(delta), TransportLogWeights(a=a, b=b, s=s, t=it))
     sol = DxgSolution(state, converged, it, seconds, trajectory, report, workers=workers)
-    if kernel.n <= dense_cap:
-        # materialize, Round (Alg. 1) and <C, pi> all on device (dxg.py:467-471)
+    if kernel.n <= dense_cap and _holds_all_rows(kernel):
+        # materialize, Round (Alg. 1) and <C, pi> all on device (dxg.py:467-471).  A row shard
+        # of a stored cost (multi-GPU runs) cannot materialize the n x n plan: no rounding then.
         P = round_on_device(_plan_on_device(state.weights, kernel, rw), rw, cw)
         out = torch.empty(1025, dtype=torch.float64, device=kernel.device)
         with torch.cuda.device(kernel.device):

@@ -127,6 +127,9 @@ class DxgEngine:
             self.world = dist.get_world_size(group)
             self.rank = dist.get_rank(group)
         r0, r1 = kernel.local_rows
+        if self.world > 1 and kernel.cost_struct().kind == _lib.COST_GRID and (r0, r1) == (0, n):
+            # grid costs: separable O(n^1.5) sweeps, replicated on every rank (see BaryEngine)
+            self.world, self.rank = 1, 0
         if self.world > 1 and (r0, r1) == (0, n):
             r0, r1 = shard_rows(n, self.world, self.rank)
         if r1 <= r0:

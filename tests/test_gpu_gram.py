@@ -18,10 +18,10 @@ from helpers import rel_err
 pytestmark = pytest.mark.gpu
 
 
-def _pair(n, d, seed):
+def _pair(n, d, seed, offset=0.0):
     from paper_2511_11359_b200 import core
     rng = np.random.default_rng(seed)
-    f = rng.random((n, d))
+    f = rng.random((n, d)) + offset
     kg = core.ColorKernel(f, 2)
     kd = core.ColorKernel(f, 2, scale=kg.scale)
     kd.norms_dev = None            # difference form
@@ -30,11 +30,14 @@ def _pair(n, d, seed):
     return kg, kd, r, c, rng
 
 
-@pytest.mark.parametrize("n,d,a", [(5001, 2, 40.0), (20000, 3, 5000.0), (4097, 1, 800.0), (6000, 4, 200.0)])
-def test_gram_iterations_track_difference_form(n, d, a):
+@pytest.mark.parametrize("n,d,a,offset", [(5001, 2, 40.0, 0.0), (20000, 3, 5000.0, 0.0), (4097, 1, 800.0, 0.0),
+                                          (6000, 4, 200.0, 0.0), (8000, 3, 2000.0, 1000.0), (3001, 2, 300.0, -250.0)])
+def test_gram_iterations_track_difference_form(n, d, a, offset):
+    """offset != 0: point clouds far from the origin (the expanded form runs on centered
+    features, so its cancellation error does not grow with |f|^2)."""
     from paper_2511_11359_b200 import dxg
     from paper_2511_11359_b200.engine import DxgEngine
-    kg, kd, r, c, rng = _pair(n, d, n + d)
+    kg, kd, r, c, rng = _pair(n, d, n + d, offset)
     prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
     delta = rng.uniform(-1, 1, n)
     b = -np.abs(rng.normal(0, 0.05 * a, n))

@@ -8,6 +8,10 @@ from torch.distributed (engine.default_group), shard the rows of the cost, and e
 2n column partials (barycenter: 2mn + the r-map normalizers) every iteration, summed in rank
 order (core.py:297-309 / dxg.py:205-207 across ranks).
 
+Grid costs (BASELINE config 5) run the separable O(n^1.5) path, which is not row-sharded:
+every rank runs the whole iteration (replicas; no per-iteration collective), so the result
+is bitwise the single-process one.
+
 Checked against the single-process run of the same instance: identical iteration counts
 and converged flags, trajectory and final state within 1e-10 (the sharded sum adds the same
 terms in a different fixed order).
@@ -47,10 +51,11 @@ def _dxg_instance(n=2048):
     return k, r, c, prm, dxg.Termination(eps=2e-3, max_iter=4000)
 
 
-def _bary_instance():
+def _bary_instance(kind="points"):
+    """points: a dense (row-sharded) barycenter; grid: the separable path (replicated per rank)."""
     from paper_2511_11359_b200 import core, dxg
     rng = np.random.default_rng(4)
-    g = core.GridKernel(12, 12, 2)
+    g = core.GridKernel(12, 12, 2) if kind == "grid" else core.ColorKernel(rng.random((150, 2)), 2)
     margs = [core.Histogram.normalized(rng.random(g.n) + 0.05) for _ in range(3)]
     prm = dxg.params_tuned(1e-2).with_overrides(tau_mu=0.05)
     return g, margs, np.array([0.2, 0.5, 0.3]), prm, dxg.Termination(eps=5e-3, max_iter=3000)
@@ -67,7 +72,7 @@ def _run(which, timeout=None):
         traj = np.array([[p.iter, p.primal, p.dual, p.col_infeas_l1] for p in sol.trajectory])
         return dict(iterations=sol.iterations, converged=sol.converged, traj=traj, delta=sol.state.mu.delta,
                     b=sol.state.weights.b)
-    g, margs, w, prm, term = _bary_instance()
+    g, margs, w, prm, term = _bary_instance("grid" if which == "bary_grid" else "points")
     sol = B.dxgb_solve(g, margs, w, prm, term, log_stride=25)
     traj = np.array([[p.iter, p.primal, p.dual, p.col_infeas_l1] for p in sol.trajectory])
     return dict(iterations=sol.iterations, converged=sol.converged, traj=traj, bary=sol.barycenter.weights,
@@ -97,7 +102,7 @@ def _spawn(which, timeout=None):
     return [dict(np.load(f"{out}_{q}.npz")) for q in range(2)]
 
 
-@pytest.mark.parametrize("which", ["dxg", "bary"])
+@pytest.mark.parametrize("which", ["dxg", "bary", "bary_grid"])
 def test_two_rank_solve_matches_single_process(which):
     ranks = _spawn(which)
     single = _run(which)
@@ -110,6 +115,8 @@ def test_two_rank_solve_matches_single_process(which):
     for key in ("delta", "b") if which == "dxg" else ("bary", "deltas"):
         assert np.array_equal(ranks[0][key], ranks[1][key])         # identical on every rank
         assert rel_err(ranks[0][key], single[key]) <= 1e-10
+        if which == "bary_grid":     # separable path replicated per rank: the same launches
+            assert np.array_equal(ranks[0][key], single[key])
 
 
 def test_two_rank_timeout_is_agreed():
