@@ -173,3 +173,26 @@ def test_config5_full_size_separable_sweep_vs_dense_samples(a):
             assert abs(col[k, j] - ref) <= 1e-11 * ref + 1e-18, (j, k)
     for k in range(m):                                      # mass: sum_j col_kj = sum_i r_i = 1
         assert abs(col[k].sum() - 1.0) <= 1e-12
+
+
+def test_config3_family_same_iteration_count_as_reference():
+    """BASELINE config 3's instance family (the bench's hash matrix, bench.py marginals, tuned +
+    tau_mu = 0.05) at n = 4096, solved to eps = 1e-4: the reference needs 12,950 iterations
+    (oracle/gen_golden_configs.py hash4096, 92 min of reference CPU); the GPU solve must stop at
+    the same logging point with the same trajectory (dxg.py:448-457)."""
+    from paper_2511_11359_b200 import core, dxg
+    d = load("hash4096_eps1e-4")
+    n = 4096
+    k = core.HashKernel(n, seed=0)
+    rng = np.random.default_rng(1)
+    rw, cw = rng.random(n), rng.random(n)
+    r, c = core.Histogram(rw / rw.sum()), core.Histogram(cw / cw.sum())
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    sol = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-4), log_stride=25, dense_cap=0)
+    assert sol.converged == bool(d["converged"])
+    assert sol.iterations == int(d["iterations"])
+    got = np.array([[p.iter, p.primal, p.dual, p.gap, p.col_infeas_l1, p.s] for p in sol.trajectory])
+    ref = d["traj"]
+    assert got.shape == ref.shape and np.array_equal(got[:, 0], ref[:, 0])
+    assert rel_err(got[:, 1], ref[:, 1]) <= 1e-8 and rel_err(got[:, 2], ref[:, 2]) <= 1e-8
+    assert rel_err(sol.state.mu.delta, d["delta"]) <= 1e-8
