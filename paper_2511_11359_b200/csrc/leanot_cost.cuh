@@ -46,13 +46,16 @@ struct CostStored {
 #pragma unroll
     for (int r = 0; r < R; ++r) { c[r][0] = p.v[r].x; c[r][1] = p.v[r].y; }
   }
-  // the column pass owns the column pairs (j, j + 1) and (j + kPairGap, j + kPairGap + 1): each
-  // 16-byte load of a warp then covers 512 contiguous bytes (whole sectors)
-  static constexpr int kPairGap = 512;
+  // four consecutive columns per thread as two 16-byte loads (j, j + 2).  Each load of a warp
+  // uses half of every 32-byte sector it touches, but the second load hits the same sectors
+  // in L1, so L2 traffic equals the algorithmic bytes (ncu lts__t_sectors_srcunit_tex_op_read
+  // = 2.52e9 = 80 GB / 32 B).  A layout with whole-sector loads per instruction (pairs at 2t and
+  // 2t + 512) removed the "excessive" L1 sectors but took 17 % more cycles (r02 A/B,
+  // profiles/r02_colpass_layout.md), so it is not used.
   struct Pre4 { double2 v0, v1; };
   __device__ __forceinline__ void pre4(const Row& row, int64_t j, Pre4& p) const {
     p.v0 = __ldcs(reinterpret_cast<const double2*>(row.p + j));
-    p.v1 = __ldcs(reinterpret_cast<const double2*>(row.p + j + kPairGap));
+    p.v1 = __ldcs(reinterpret_cast<const double2*>(row.p + j + 2));
   }
   // four consecutive columns (j % 4 == 0 not required; j even), for the column pass
   struct Col4 {};

@@ -732,26 +732,40 @@ struct RowOwnerFn {
   int run() {
     auto kern = dxg_rowowner_kernel<COST>;
     const size_t smem = TAB_BYTES + 2 * PO_MAX_N * 8 + (size_t)PO_R * a_n(P) * 8;
-    static bool attr = false;  // per instantiation
-    if (!attr) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    // the shared-memory size depends on the plan (cached cost rows): raise the kernel's limit
+    // whenever a plan needs more than the largest one so far (a first, smaller plan must not
+    // cap later ones -- that made the occupancy query return 0 for a larger n)
+    static size_t attr_smem = 0;  // per instantiation
+    if (smem > attr_smem) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        set_error("row-owner: shared memory attribute");
         return LEANOT_EINVAL;
-      attr = true;
+      }
+      attr_smem = smem;
     }
     PersistArgs a = P;
     const int64_t n = a.U.n;
     const int G = num_sms();
-    if ((n + G - 1) / G > PO_R || n > PO_MAX_N || G > PO_LPV * PO_PARTS) return LEANOT_EINVAL;
-    if ((int64_t)G * 2 * n + 6 * G > slab_doubles) return LEANOT_EINVAL;
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PO_THREADS, smem) != cudaSuccess || occ < 1)
+    if ((n + G - 1) / G > PO_R || n > PO_MAX_N || G > PO_LPV * PO_PARTS) {
+      set_error("row-owner: n = %lld does not fit %d CTAs", (long long)n, G);
       return LEANOT_EINVAL;
+    }
+    if ((int64_t)G * 2 * n + 6 * G > slab_doubles) {
+      set_error("row-owner: slab of %lld doubles < %lld", (long long)slab_doubles, (long long)(G * 2 * n + 6 * G));
+      return LEANOT_EINVAL;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PO_THREADS, smem) != cudaSuccess || occ < 1) {
+      set_error("row-owner: occupancy query failed (occ %d)", occ);
+      return LEANOT_EINVAL;
+    }
     a.gmax = a.slab + (int64_t)G * 2 * n;
     a.epart = a.gmax + G;
     void* args[] = {&a};
     const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, G, PO_THREADS, args, smem, st);
     if (e != cudaSuccess) {
       cudaGetLastError();
+      set_error("row-owner: cooperative launch: %s", cudaGetErrorString(e));
       return LEANOT_EINVAL;
     }
     return LEANOT_OK;
@@ -801,22 +815,15 @@ struct PersistFn {
 };
 
 // LEANOT_ROWOWNER=0 keeps the four-barrier persistent kernel for n <= 1024 (A/B comparisons)
+// read on every call (not cached): tests switch these paths per test with the environment
 static bool rowowner_env() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("LEANOT_ROWOWNER");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  const char* e = getenv("LEANOT_ROWOWNER");
+  return !(e && e[0] == '0');
 }
 
 static bool persist_env() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("LEANOT_PERSIST");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  const char* e = getenv("LEANOT_PERSIST");
+  return !(e && e[0] == '0');
 }
 
 // Runs `iters` iterations persistently when the plan qualifies; returns LEANOT_OK if it did,

@@ -1012,9 +1012,10 @@ int leanot_dxg_iterate(const leanot_dxg_plan_t* P, int iters, void* stream) {
 int leanot_dxg_iterate_eval(const leanot_dxg_plan_t* P, int iters, int start_update, void* stream) {
   LEANOT_TRY(validate_plan(P));
   LEANOT_TRY(ensure_init());
+  g_err[0] = 0;
   const int rc = try_rowowner_iterate_eval(*P, iters, start_update, S_(stream));
   if (rc != LEANOT_OK) {
-    set_error("dxg_iterate_eval: plan not eligible (single-process, n <= 1024, non-separable cost)");
+    if (!g_err[0]) set_error("dxg_iterate_eval: plan not eligible (single-process, n <= 1024, non-separable cost)");
     return rc;
   }
   return check_launch("dxg_iterate_eval");

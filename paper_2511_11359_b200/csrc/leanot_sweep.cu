@@ -369,16 +369,8 @@ __global__ void __launch_bounds__(CP_THREADS, LEANOT_CP_MINB) colpass_kernel(con
 #pragma unroll
   for (int k = 0; k < K; ++k) mult[k] = COST::kGram ? 2.0 * A.a[k] * A.cost.inv_scale : -A.a[k];
 
-  // Columns of this thread: 4 consecutive ones (on-the-fly costs), or for the stored cost two
-  // pairs 512 apart (CostStored::kPairGap) so that every 16-byte load of a warp reads whole
-  // 32-byte sectors (4 consecutive doubles per lane would use half of each sector per load).
-  auto colv = [&](int64_t tile, int v) -> int64_t {
-    if constexpr (COST::kStored)
-      return tile * CP_TILE + 2 * threadIdx.x + (v >> 1) * COST::kPairGap + (v & 1);
-    else
-      return tile * CP_TILE + CP_V * threadIdx.x + v;
-  };
-  static_assert(!COST::kStored || 2 * COST::kPairGap == CP_TILE, "stored column pass layout");
+  // columns of this thread: CP_V consecutive ones
+  auto colv = [&](int64_t tile, int v) -> int64_t { return tile * CP_TILE + CP_V * threadIdx.x + v; };
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t tile = it % ntiles, split = it / ntiles;
     const int64_t j = colv(tile, 0);
