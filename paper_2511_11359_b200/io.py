@@ -67,13 +67,20 @@ def read_pgm(path) -> np.ndarray:
     return px.reshape(height, width)
 
 
-def write_pgm(path, pixels, maxval: int = 255) -> None:
-    """Binary P5, [0, max(pixels)] mapped linearly to [0, maxval] and rounded half-to-even."""
+def write_pgm(path, pixels, maxval: int = 255, rescale: bool = True) -> None:
+    """Binary P5, [0, max(pixels)] mapped linearly to [0, maxval] and rounded half-to-even.
+
+    rescale=False writes the values as they are (rounded, clipped to [0, maxval]): the
+    reference CLI's `downsample` passes it (cli.py:397) but its write_pgm lacks the
+    parameter; the default keeps the reference behaviour."""
     img = np.asarray(pixels, dtype=float)
     if img.ndim != 2:
         raise ValueError("expected a 2-D image")
     peak = img.max()
-    q = np.zeros(img.shape) if peak <= 0 else img / peak * maxval
+    if not rescale:
+        q = img
+    else:
+        q = np.zeros(img.shape) if peak <= 0 else img / peak * maxval
     q = np.clip(np.rint(q), 0, maxval).astype(">u2" if maxval >= 256 else "u1")
     head = b"P5\n%d %d\n%d\n" % (img.shape[1], img.shape[0], maxval)
     with open(path, "wb") as fh:
