@@ -30,6 +30,24 @@ def _torch():
     return torch
 
 
+# NVTX ranges around the engine phases (sweep / update / evaluate / iterate) for nsys-style
+# timelines: LEANOT_NVTX=1 (off by default: a range push/pop per launch costs a few us)
+_NVTX = os.environ.get("LEANOT_NVTX", "0") == "1"
+
+
+class _nvtx:
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if _NVTX:
+            _torch().cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *a):
+        if _NVTX:
+            _torch().cuda.nvtx.range_pop()
+
+
 def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous row shard of rank `rank` (ceil split; trailing ranks may be shorter)."""
     per = (n + world - 1) // world
@@ -250,7 +268,7 @@ class DxgEngine:
             flags |= 32
         elif single_read is False:
             flags |= 16
-        with _torch().cuda.device(self.device):
+        with _nvtx("leanot.sweep.eval" if evaluate else "leanot.sweep"), _torch().cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_sweep(C.byref(self.plan), flags, self._stream()), "dxg_sweep")
         if self.world > 1:
             self._combine_cols()
@@ -267,7 +285,7 @@ class DxgEngine:
         self.col.copy_(combine_partials(self.col, self.group, self.world))
 
     def update(self):
-        with _torch().cuda.device(self.device):
+        with _nvtx("leanot.update"), _torch().cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_update(C.byref(self.plan), self._stream()), "dxg_update")
 
     def iterate(self, iters: int, use_graph: bool | None = None):
@@ -299,7 +317,7 @@ class DxgEngine:
     def evaluate(self):
         """(primal, dual, infeas, s) of the state swept by the last sweep(evaluate=True)."""
         torch = _torch()
-        with torch.cuda.device(self.device):
+        with _nvtx("leanot.eval"), torch.cuda.device(self.device):
             _lib.check(_lib.lib().leanot_dxg_eval(C.byref(self.plan), self._stream()), "dxg_eval")
         # the scalars (a, a_bar, s, t) travel in the same device->host transfer
         self.evalbuf[8:12].copy_(self.scal[:4])
