@@ -186,18 +186,25 @@ def cpu_reference(n, seed, steps, warmup):
 
 
 def init_dist(args):
+    """One process per GPU (torchrun env).  LEANOT_BENCH_BACKEND=gloo (tests only) runs the ranks
+    on whatever GPUs exist, possibly all on one, with host-staged collectives."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    backend = os.environ.get("LEANOT_BENCH_BACKEND", "nccl")
+    dev = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(dev)
     group = None
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
-    return world, rank, local, group
+    return world, rank, dev, group
 
 
 def barrier(group):
@@ -211,7 +218,8 @@ def max_over_ranks(x, group):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
 
@@ -291,7 +299,7 @@ def run_b200(args):
     ms_per_step = 1e3 * elapsed_max / K
 
     peak, peak_kind = hbm_peak()
-    bytes_alg = 8.0 * n * nr                       # one read of the local rows of C per iteration
+    bytes_alg = 8.0 * n * nr                       # one read of this rank's rows of C per iteration (per-GPU roofline)
     t_sweep = statistics.mean(t_rows) + statistics.mean(t_cols)
     # dominant kernel = pass B (column sums); report it and the whole sweep
     t_colk = statistics.mean(t_cols)
@@ -323,7 +331,7 @@ def run_b200(args):
                      "update": 1e3 * statistics.mean(t_upd)},
     }
     prof = ROOT / "profiles" / "traffic.json"
-    if prof.exists():
+    if prof.exists() and world == 1:      # the capture is of the single-GPU (all rows) launch
         try:
             tj = json.loads(prof.read_text())
             roofline["traffic"] = tj.get("colpass_dram_bytes_per_launch")
