@@ -139,7 +139,7 @@ class BaryEngine:
         self.r = z(2 * n)
         self.coef = z(8 * m * n)
         self.rowstat = z(3 * m * n)
-        slab = splits * 2 * n
+        slab = splits * 4 * n     # pass B of two marginals at once (K = 4 weight sets, leanot_bary.cu)
         if kernel.cost_struct().kind == _lib.COST_GRID:   # separable path scratch (leanot_sep.cu)
             cs = kernel.cost_struct()
             slab = max(slab, int(L.leanot_grid_sep_ws_doubles(cs)) + 5 * m * n + m * max(cs.height, cs.width))

@@ -124,6 +124,28 @@ static RowPassArgs bary_rowpass(const leanot_bary_plan_t& P, int k) {
   return A;
 }
 
+// marginals k and k + 1 in one pass A: sets {0, 1} = marginal k (now, bar), {2, 3} = k + 1
+static RowPassArgs bary_rowpass2(const leanot_bary_plan_t& P, int k) {
+  RowPassArgs A = bary_rowpass(P, k);
+  const int64_t nr = P.row1 - P.row0;
+  A.a = P.scal + 4;                               // [a, a_bar, a, a_bar] (bary_a4_kernel)
+  A.b[2] = P.b + (k + 1) * P.ns; A.b[3] = P.b_bar + (k + 1) * P.ns;
+  A.shift_kstride = nr; A.shift_kgroup = 2;       // marginal k + set / 2
+  A.next_group = 2;                               // sets 1, 3 -> next shifts of k, k + 1
+  A.rowstat = nullptr;
+  return A;
+}
+
+__global__ void bary_a4_kernel(double* scal) {
+  if (threadIdx.x < 4) scal[4 + threadIdx.x] = scal[threadIdx.x & 1];
+}
+
+// LEANOT_BARY_BATCH=0: one marginal per pass (A/B measurements); read per call
+static int bary_batch() {
+  const char* e = getenv("LEANOT_BARY_BATCH");
+  return (e && e[0] == '0') ? 1 : 2;
+}
+
 }  // namespace leanot
 
 extern "C" {
@@ -169,9 +191,19 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
     LEANOT_TRY(sep_bary_cols(*P, st));
     return check_launch("bary_sweep(separable)");
   }
-  for (int k = 0; k < m; ++k) {
-    RowPassArgs A = bary_rowpass(*P, k);
-    LEANOT_TRY(launch_rowpass(A, 2, (flags & LEANOT_SWEEP_EVAL) != 0, st));
+  // plain sweeps: two marginals per launch (K = 4 weight sets {b_k, b_bar_k, b_k+1, b_bar_k+1}
+  // share each read of C; a, a_bar mirrored into scal[4..7]); evaluation sweeps: one per marginal
+  const bool eval = (flags & LEANOT_SWEEP_EVAL) != 0;
+  const int kb = eval ? 1 : bary_batch();
+  if (kb == 2) bary_a4_kernel<<<1, 32, 0, st>>>(P->scal);
+  for (int k = 0; k < m; k += kb) {
+    if (kb == 2 && k + 1 < m) {
+      RowPassArgs A = bary_rowpass2(*P, k);
+      LEANOT_TRY(launch_rowpass(A, 4, false, st));
+    } else {
+      RowPassArgs A = bary_rowpass(*P, k);
+      LEANOT_TRY(launch_rowpass(A, 2, eval, st));
+    }
   }
   const int64_t tot = (int64_t)m * 2 * nr;
   const int g = (int)std::min<int64_t>((tot + 255) / 256, 4096);
@@ -180,15 +212,20 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
   for (int w = 0; w < 2; ++w)
     launch_rmap(P->L + (int64_t)w * m * nr, m, n, P->w, P->scratch, P->partial, P->r + (int64_t)w * n, st);
   bary_coef_kernel<<<g, 256, 0, st>>>(P->S, P->r, m, nr, P->row0, n, P->coef);
-  for (int k = 0; k < m; ++k) {
+  // column sums: two marginals per launch as well (the per-set m / coef / col blocks of
+  // marginals k and k + 1 are contiguous, so K = 4 indexes straight through them)
+  const int cb = bary_batch();
+  for (int k = 0; k < m; k += cb) {
+    const int K = cb == 2 && k + 1 < m ? 4 : 2;
     ColPassArgs B;
     memset(&B, 0, sizeof(B));
-    B.cost = make_view(P->cost); B.i0 = P->row0; B.i1 = P->row1; B.a = P->scal;
+    B.cost = make_view(P->cost); B.i0 = P->row0; B.i1 = P->row1; B.a = K == 4 ? P->scal + 4 : P->scal;
     B.b[0] = P->b + k * P->ns; B.b[1] = P->b_bar + k * P->ns;
+    if (K == 4) { B.b[2] = P->b + (k + 1) * P->ns; B.b[3] = P->b_bar + (k + 1) * P->ns; }
     B.m = P->mu + (int64_t)k * 2 * nr; B.coef = P->coef + (int64_t)k * 2 * nr * 4; B.slab = P->slab;
     B.splits = P->splits;
-    LEANOT_TRY(launch_colpass(B, 2, st));
-    LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, n, P->col + (int64_t)k * 2 * n, st));
+    LEANOT_TRY(launch_colpass(B, K, st));
+    LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, K, n, P->col + (int64_t)k * 2 * n, st));
   }
   return check_launch("bary_sweep");
 }
@@ -243,9 +280,19 @@ int leanot_bary_rows(const leanot_bary_plan_t* P, int flags, double* gmax, void*
   cudaStream_t st = S_(stream);
   const int64_t n = P->n, nr = P->row1 - P->row0;
   const int m = P->m;
-  for (int k = 0; k < m; ++k) {
-    RowPassArgs A = bary_rowpass(*P, k);
-    LEANOT_TRY(launch_rowpass(A, 2, (flags & LEANOT_SWEEP_EVAL) != 0, st));
+  // plain sweeps: two marginals per launch (K = 4 weight sets {b_k, b_bar_k, b_k+1, b_bar_k+1}
+  // share each read of C; a, a_bar mirrored into scal[4..7]); evaluation sweeps: one per marginal
+  const bool eval = (flags & LEANOT_SWEEP_EVAL) != 0;
+  const int kb = eval ? 1 : bary_batch();
+  if (kb == 2) bary_a4_kernel<<<1, 32, 0, st>>>(P->scal);
+  for (int k = 0; k < m; k += kb) {
+    if (kb == 2 && k + 1 < m) {
+      RowPassArgs A = bary_rowpass2(*P, k);
+      LEANOT_TRY(launch_rowpass(A, 4, false, st));
+    } else {
+      RowPassArgs A = bary_rowpass(*P, k);
+      LEANOT_TRY(launch_rowpass(A, 2, eval, st));
+    }
   }
   const int64_t tot = (int64_t)m * 2 * nr;
   const int g = (int)std::min<int64_t>((tot + 255) / 256, 4096);
@@ -288,15 +335,19 @@ int leanot_bary_cols(const leanot_bary_plan_t* P, const double* esum, void* stre
   const int64_t tot = (int64_t)m * 2 * nr;
   const int g = (int)std::min<int64_t>((tot + 255) / 256, 4096);
   bary_coef_kernel<<<g, 256, 0, st>>>(P->S, P->r, m, nr, P->row0, n, P->coef);
-  for (int k = 0; k < m; ++k) {
+  bary_a4_kernel<<<1, 32, 0, st>>>(P->scal);
+  const int cb = bary_batch();
+  for (int k = 0; k < m; k += cb) {   // two marginals per read of C (as leanot_bary_sweep)
+    const int K = cb == 2 && k + 1 < m ? 4 : 2;
     ColPassArgs B;
     memset(&B, 0, sizeof(B));
-    B.cost = make_view(P->cost); B.i0 = P->row0; B.i1 = P->row1; B.a = P->scal;
+    B.cost = make_view(P->cost); B.i0 = P->row0; B.i1 = P->row1; B.a = K == 4 ? P->scal + 4 : P->scal;
     B.b[0] = P->b + k * P->ns; B.b[1] = P->b_bar + k * P->ns;
+    if (K == 4) { B.b[2] = P->b + (k + 1) * P->ns; B.b[3] = P->b_bar + (k + 1) * P->ns; }
     B.m = P->mu + (int64_t)k * 2 * nr; B.coef = P->coef + (int64_t)k * 2 * nr * 4; B.slab = P->slab;
     B.splits = P->splits;
-    LEANOT_TRY(launch_colpass(B, 2, st));
-    LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, 2, n, P->col + (int64_t)k * 2 * n, st));
+    LEANOT_TRY(launch_colpass(B, K, st));
+    LEANOT_TRY(launch_slab_reduce(P->slab, P->splits, K, n, P->col + (int64_t)k * 2 * n, st));
   }
   return check_launch("bary_cols");
 }

@@ -13,8 +13,9 @@ struct RowPassArgs {
   int64_t i0, i1;              // global rows [i0, i1)
   const double* a;             // K device scalars
   const double* b[LEANOT_MAX_K];
-  const int64_t* shift;        // shift[k*shift_kstride + (i-i0)]
+  const int64_t* shift;        // shift[(k / shift_kgroup) * shift_kstride + (i-i0)] (shift_at)
   int64_t shift_kstride;       // 0: one shift per row shared by all weight sets
+  int shift_kgroup;            // weight sets per shift group (0 or 1: every set its own stride)
   double* S;                   // K x nr row sums
   int64_t* m_used;             // K x nr shifts used (may be null)
   // evaluation sweep (weight set 0)
@@ -25,6 +26,8 @@ struct RowPassArgs {
   double* coef;                // K x nr x 4 (may be null)
   int64_t* shift_next;         // nr (may be null)
   int next_from_k;
+  int next_group;              // > 0: sets k with k % next_group == next_from_k write
+                               // shift_next[(k / next_group) * nr + li] (batched barycenter marginals)
   int32_t* flags;              // [count, -, (k, li)...]
   int gram;                    // 1: points p = 2 with norms -> expanded-form sweep (CostGram)
 };
@@ -40,6 +43,12 @@ struct ColPassArgs {
   int splits;
   int gram;                    // must match the pass A that produced m / coef
 };
+
+// row shift of weight set k, local row li
+__host__ __device__ inline int64_t shift_at(const RowPassArgs& A, int k, int64_t li) {
+  const int g = A.shift_kgroup > 1 ? k / A.shift_kgroup : k;
+  return A.shift[g * A.shift_kstride + li];
+}
 
 int num_sms();
 bool gram_enabled();

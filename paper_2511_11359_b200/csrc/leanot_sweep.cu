@@ -71,7 +71,8 @@ __device__ __forceinline__ void finalize_row(const RowPassArgs& A, int k, int64_
     double* cf = A.coef + (k * nr + li) * 4;
     cf[0] = g * EC0; cf[1] = g * EC1; cf[2] = g * EC2; cf[3] = g * EC3;
   }
-  if (A.shift_next && k == A.next_from_k) A.shift_next[li] = m + llrint(log(S) * (1.0 / LSTEP));
+  if (A.shift_next && (A.next_group > 0 ? k % A.next_group == A.next_from_k : k == A.next_from_k))
+    A.shift_next[(A.next_group > 0 ? (int64_t)(k / A.next_group) * nr : 0) + li] = m + llrint(log(S) * (1.0 / LSTEP));
 }
 
 template <class COST, int K, int R, bool EVAL>
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
       rows[r] = cost.row(i);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        int64_t sh = A.shift[k * A.shift_kstride + (i - A.i0)];
+        int64_t sh = shift_at(A, k, i - A.i0);
         if constexpr (COST::kGram) sh -= gram_off(A.a[k], A.cost.inv_scale, cost.norm(i));
         mlo[r][k] = (uint32_t)sh;
       }
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(RP_THREADS, LEANOT_RP_MINB) rowpass_kernel(con
         const int r = v / K, k = v % K;
         const int64_t i = ib + r;
         if (i < rb1) {
-          const int64_t m = A.shift[k * A.shift_kstride + (i - A.i0)];
+          const int64_t m = shift_at(A, k, i - A.i0);
           int64_t mu = m;
           if constexpr (COST::kGram) mu -= gram_off(A.a[k], A.cost.inv_scale, cost.norm(i));
           finalize_row(A, k, i - A.i0, t, m, mu);
@@ -303,7 +304,9 @@ __global__ void __launch_bounds__(1024) fixup_kernel(const RowPassArgs A) {
       // expanded form: m is in the x' convention; the stored shift is in the x convention
       int64_t off = 0;
       if constexpr (COST::kGram) off = gram_off(A.a[k], A.cost.inv_scale, cost.norm(i));
-      if (A.shift_next && k == A.next_from_k) A.shift_next[li] = m + off + llrint(log(t) * (1.0 / LSTEP));
+      if (A.shift_next && (A.next_group > 0 ? k % A.next_group == A.next_from_k : k == A.next_from_k))
+        A.shift_next[(A.next_group > 0 ? (int64_t)(k / A.next_group) * nr : 0) + li] =
+            m + off + llrint(log(t) * (1.0 / LSTEP));
     }
     __syncthreads();
   }
@@ -731,9 +734,10 @@ struct RowPassFn {
       }
     }
     if constexpr (std::is_same<COST, CostStored>::value) {
-      if (tma_ok(A.cost) && (K == 1 || K == 2)) {
+      if (tma_ok(A.cost) && (K == 1 || K == 2 || (K == 4 && !eval))) {
         if (K == 1) rc = eval ? launch_rowpass_tma_t<1, 4, true>(A, st) : launch_rowpass_tma_t<1, 4, false>(A, st);
-        else rc = eval ? launch_rowpass_tma_t<2, 4, true>(A, st) : launch_rowpass_tma_t<2, 4, false>(A, st);
+        else if (K == 2) rc = eval ? launch_rowpass_tma_t<2, 4, true>(A, st) : launch_rowpass_tma_t<2, 4, false>(A, st);
+        else rc = launch_rowpass_tma_t<4, 2, false>(A, st);   // two barycenter marginals per read of C
         if (rc != LEANOT_OK) return rc;
         if (A.flags) return launch_fixup_t<COST>(A, st);
         return LEANOT_OK;
@@ -741,6 +745,7 @@ struct RowPassFn {
     }
     if (K == 1) rc = eval ? launch_rowpass_t<COST, 1, R, true>(A, st) : launch_rowpass_t<COST, 1, R, false>(A, st);
     else if (K == 2) rc = eval ? launch_rowpass_t<COST, 2, R, true>(A, st) : launch_rowpass_t<COST, 2, R, false>(A, st);
+    else if (K == 4 && !eval) rc = launch_rowpass_t<COST, 4, 2, false>(A, st);
     else return LEANOT_EINVAL;
     if (rc != LEANOT_OK) return rc;
     if (A.flags) return launch_fixup_t<COST>(A, st);
@@ -820,6 +825,7 @@ struct ColPassFn {
     }
     if (K == 1) return launch_colpass_t<COST, 1>(A, st);
     if (K == 2) return launch_colpass_t<COST, 2>(A, st);
+    if (K == 4) return launch_colpass_t<COST, 4>(A, st);
     return LEANOT_EINVAL;
   }
 };

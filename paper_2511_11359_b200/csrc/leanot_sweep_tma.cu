@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
     for (int r = 0; r < R; ++r) {
       const int64_t i = ib + r < A.i1 ? ib + r : A.i1 - 1;
 #pragma unroll
-      for (int k = 0; k < K; ++k) mlo[r][k] = (uint32_t)A.shift[k * A.shift_kstride + (i - A.i0)];
+      for (int k = 0; k < K; ++k) mlo[r][k] = (uint32_t)shift_at(A, k, i - A.i0);
     }
     double acc[R][K], U[R], V[R], mn[R];
 #pragma unroll
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(TP_ALL, 1) rowpass_tma_kernel(const RowPassArg
         const int r = v / K, k = v % K;
         const int64_t i = ib + r;
         if (i < A.i1) {
-          const int64_t m = A.shift[k * A.shift_kstride + (i - A.i0)];
+          const int64_t m = shift_at(A, k, i - A.i0);
           finalize_row(A, k, i - A.i0, t, m, m);
         }
       } else if (EVAL) {
