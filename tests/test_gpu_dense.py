@@ -66,8 +66,29 @@ def test_solve_with_rounding_is_feasible():
     assert np.abs(P.sum(axis=0) - d["c"]).sum() <= 1e-12
     Cn = d["k_C"] / d["k_C"].max()
     assert abs(sol.rounded_cost - float((P * Cn).sum())) <= 1e-13
-    # the oracle's Round of the same final plan (clamped deficits) agrees
+    # Round of the same final plan on the host: the device clamps the deficits dr, dc at 0
+    # before the rank-one correction (rounding.py:80-87 can produce tiny negative entries,
+    # SURVEY.md Appendix B-5), so compare with that rule always, and with the reference's rule
+    # whenever the reference's result is a valid coupling (then the two rules coincide)
     w = sol.state.weights
     plan = dxg.materialize_plan(w, k, d["r"])
-    assert rel_err(P, O.round_to_polytope(plan, d["r"], d["c"]) if np.all(
-        O.round_to_polytope(plan, d["r"], d["c"]) >= 0) else P) <= 1e-12
+    assert rel_err(P, _round_clamped(plan, d["r"], d["c"])) <= 1e-12
+    ref = O.round_to_polytope(plan, d["r"], d["c"])
+    if np.all(ref >= 0):
+        assert rel_err(P, ref) <= 1e-12
+
+
+def _round_clamped(m, r, c):
+    """Alg. 1 (rounding.py:63-87) with the missing-mass vectors clamped at 0 (the device rule)."""
+    row = m.sum(axis=1)
+    x = np.where(row > 0, np.minimum(r / np.where(row > 0, row, 1.0), 1.0), 1.0)
+    m = m * x[:, None]
+    col = m.sum(axis=0)
+    y = np.where(col > 0, np.minimum(c / np.where(col > 0, col, 1.0), 1.0), 1.0)
+    m = m * y[None, :]
+    dr = np.maximum(r - m.sum(axis=1), 0.0)
+    dc = np.maximum(c - m.sum(axis=0), 0.0)
+    mass = dr.sum()
+    if mass > O.MASS_EPS:
+        m = m + np.outer(dr, dc) / mass
+    return m
