@@ -197,17 +197,31 @@ def sinkhorn_column_marginal(pot: DualPotentials, kernel, workers: int = 1) -> n
         return col.cpu().numpy()
 
 
+def _potential_plan(kernel, phi, psi, eta: float):
+    """exp((phi_i + psi_j - C_ij) / eta) as a device n x n tensor, by the implicit-plan kernel
+    (leanot_materialize_plan: r_i exp(-(a C_ij + b_j) - L_i) with a = 1/eta, b = -psi/eta,
+    r = 1, L = -phi/eta): the cost is evaluated on device, no dense host copy of C."""
+    torch = _torch()
+    dev = kernel.device
+    n = kernel.n
+    with torch.cuda.device(dev):
+        b = torch.as_tensor(-np.asarray(psi, dtype=float) / eta, device=dev)
+        L = torch.as_tensor(-np.asarray(phi, dtype=float) / eta, device=dev)
+        ones = torch.ones(n, dtype=torch.float64, device=dev)
+        P = torch.empty((n, n), dtype=torch.float64, device=dev)
+        _lib.check(_lib.lib().leanot_materialize_plan(kernel.cost_struct(), 1.0 / eta, b.data_ptr(), ones.data_ptr(),
+                                                      L.data_ptr(), P.data_ptr(), n, _lib.stream_handle()),
+                   "materialize_plan")
+    return P
+
+
 def sinkhorn_plan_dense(pot: DualPotentials, kernel, cap: int = DENSE_CAP) -> np.ndarray:
     """Normalized dense plan, n <= cap (sinkhorn.py:153-159)."""
     kernel = as_device_kernel(kernel)
     if kernel.n > cap:
         raise ValueError("plan materialization above the dense cap")
-    torch = _torch()
-    dev = kernel.device
-    Cm = torch.from_numpy(kernel.materialize(cap)).to(dev)
-    z = (torch.as_tensor(pot.phi, device=dev)[:, None] + torch.as_tensor(pot.psi, device=dev)[None, :] - Cm) / pot.eta
-    plan = torch.exp(z)
-    return (plan / plan.sum()).cpu().numpy()
+    plan = _potential_plan(kernel, pot.phi, pot.psi, pot.eta).cpu().numpy()
+    return plan / plan.sum()
 
 
 def ibp_barycenter(kernel, marginals, weights, eta: float, tol: float = 1e-9, max_iter: int = 10_000,
@@ -269,9 +283,4 @@ def ibp_plan_dense(res: IbpResult, kernel, k: int, cap: int = DENSE_CAP) -> np.n
     kernel = as_device_kernel(kernel)
     if kernel.n > cap:
         raise ValueError("plan materialization above the dense cap")
-    torch = _torch()
-    dev = kernel.device
-    Cm = torch.from_numpy(kernel.materialize(cap)).to(dev)
-    z = (torch.as_tensor(res.phis[k], device=dev)[:, None] + torch.as_tensor(res.psis[k], device=dev)[None, :]
-         - Cm) / res.eta
-    return torch.exp(z).cpu().numpy()
+    return _potential_plan(kernel, res.phis[k], res.psis[k], res.eta).cpu().numpy()

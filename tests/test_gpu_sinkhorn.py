@@ -78,3 +78,24 @@ def test_grid_separable_sinkhorn_and_ibp_match_dense(eta):
     bd = SK.ibp_barycenter(e, margs, [0.2, 0.3, 0.5], eta, tol=1e-9, max_iter=200)
     assert bs.sweeps == bd.sweeps
     assert rel_err(bs.barycenter.weights, bd.barycenter.weights) <= 1e-9
+
+
+def test_dense_plans_match_numpy_from_potentials():
+    """sinkhorn_plan_dense / ibp_plan_dense (sinkhorn.py:153-159, 231-236) through the device
+    plan kernel agree with exp((phi + psi - C) / eta) computed on the host."""
+    from paper_2511_11359_b200 import core
+    from paper_2511_11359_b200 import sinkhorn as sk
+    rng = np.random.default_rng(12)
+    n = 90
+    Cm = rng.random((n, n))
+    k = core.ExplicitKernel(Cm)
+    r = core.Histogram.normalized(rng.random(n) + 0.1)
+    c = core.Histogram.normalized(rng.random(n) + 0.1)
+    pot = sk.sinkhorn_solve(k, r, c, 0.05, tol=1e-10, max_iter=5000)
+    Cn = Cm / Cm.max()
+    ref = np.exp((pot.phi[:, None] + pot.psi[None, :] - Cn) / pot.eta)
+    assert rel_err(sk.sinkhorn_plan_dense(pot, k), ref / ref.sum()) <= 1e-12
+    res = sk.ibp_barycenter(k, [r, c], np.array([0.4, 0.6]), 0.05, tol=1e-9, max_iter=2000)
+    for q in range(2):
+        ref = np.exp((res.phis[q][:, None] + res.psis[q][None, :] - Cn) / res.eta)
+        assert rel_err(sk.ibp_plan_dense(res, k, q), ref) <= 1e-12
