@@ -100,9 +100,17 @@ def config4(shards=8):
     # dot product 3 (DMUL + 2 DFMA) + per weight set: x' 1 + table exp 7 (incl. the accumulate)
     per_elem = 2 * (3 + 2 * 8)
     fp64 = per_elem * n * (r1 - r0) / per_iter
+    # SURVEY.md §8(d) algorithmic count for config 4: 47 FP64 instructions per element and
+    # iteration (single-read ideal with libdevice exps); reported beside the executed count
+    alg = 47 * n * (r1 - r0) / per_iter
     return {"config": 4, "n": n, "rows_this_gpu": r1 - r0, "shards": shards, "seconds_per_iter_per_gpu": per_iter,
             "projected_iters_per_s_8gpu": 1.0 / per_iter, "fp64_instr_per_s": fp64,
             "fp64_instr_per_element_iter": per_elem, "fp64_frac_of_measured_dfma_peak": fp64 / 17.07e12,
+            "fp64_frac_survey_count": alg / 17.07e12,
+            "fp64_definitions": "executed: 38 FP64 instructions per element and iteration in the two-pass "
+                                "expanded form (what the kernels issue); survey: SURVEY.md §8(d)'s 47 per element "
+                                "(single-read, libdevice exp); peak: builder DFMA microbenchmark 17.07e12/s at "
+                                "1965 MHz (profiles/r01_microbench.md), not in MEASURED_PEAKS.json",
             "note": "1 GPU runs one 1/8 row shard; the 8-GPU run adds one 16 MB all-gather per iteration"}
 
 
