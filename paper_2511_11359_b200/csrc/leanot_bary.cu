@@ -213,8 +213,10 @@ int leanot_bary_sweep(const leanot_bary_plan_t* P, int flags, void* stream) {
     launch_rmap(P->L + (int64_t)w * m * nr, m, n, P->w, P->scratch, P->partial, P->r + (int64_t)w * n, st);
   bary_coef_kernel<<<g, 256, 0, st>>>(P->S, P->r, m, nr, P->row0, n, P->coef);
   // column sums: two marginals per launch as well (the per-set m / coef / col blocks of
-  // marginals k and k + 1 are contiguous, so K = 4 indexes straight through them)
+  // marginals k and k + 1 are contiguous, so K = 4 indexes straight through them).  The
+  // [a, a_bar, a, a_bar] copy is refreshed here too: evaluation sweeps skip the pass-A one.
   const int cb = bary_batch();
+  if (cb == 2) bary_a4_kernel<<<1, 32, 0, st>>>(P->scal);
   for (int k = 0; k < m; k += cb) {
     const int K = cb == 2 && k + 1 < m ? 4 : 2;
     ColPassArgs B;

@@ -70,3 +70,24 @@ def test_batched_matches_one_marginal_per_pass(monkeypatch):
         out.append((eng.col.cpu().numpy().copy(), eng.delta.cpu().numpy().copy()))
     assert rel_err(out[0][0], out[1][0]) <= 1e-12
     assert rel_err(out[0][1], out[1][1]) <= 1e-11
+
+
+def test_batched_evaluation_sweep_matches_oracle():
+    """Evaluation sweeps (one marginal per pass A, pairs in pass B) after plain iterations: the
+    pair pass B must see the current (a, a_bar), not the last plain sweep's copy."""
+    from paper_2511_11359_b200 import barycenter as B
+    from paper_2511_11359_b200 import core, dxg
+    k, cost, margs, w, deltas, bs = _inst("stored", 4, 21)
+    prm = dxg.params_tuned(1e-2).with_overrides(tau_mu=0.05)
+    eng = B.BaryEngine(k, [core.Histogram(h) for h in margs], w, prm)
+    eng.load_state(deltas, bs, 9.0, 0.01, 9)
+    for _ in range(3):
+        eng.sweep()
+        eng.update()
+    d2, b2, a2, s2, t2 = eng.read_state()
+    eng.sweep(evaluate=True)
+    primal, dual, infeas = eng.evaluate()
+    ref = O.bary_evaluate(O.BaryIterate(d2, b2, a2, s2, t2, w, prm.eta), cost, margs)
+    assert abs(primal - ref[0]) <= 1e-10 * max(1.0, abs(ref[0]))
+    assert abs(dual - ref[1]) <= 1e-10 * max(1.0, abs(ref[1]))
+    assert rel_err(np.asarray(infeas), np.asarray(ref[2])) <= 1e-9
