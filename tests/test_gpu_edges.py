@@ -26,7 +26,7 @@ def test_tiny_and_boundary_sizes_track_oracle(n):
                     log_stride=25, dense_cap=0)
     it, conv, iters, traj, col = O.solve(O.DenseCost(Cm), r, c, O.params_tuned(0.0, tau_mu=0.05), eps=1e-12,
                                           max_iter=60)
-    assert sol.iterations == iters == 60
+    assert sol.iterations == iters and sol.converged == conv     # n = 1 converges at the first log point
     assert rel_err(sol.state.mu.delta, it.delta) <= 1e-10
     assert rel_err(sol.state.weights.b, it.b) <= 1e-10
     assert abs(sol.final.primal - traj[-1][1]) <= 1e-9 * max(1.0, abs(traj[-1][1]))
