@@ -44,7 +44,7 @@ constexpr int SR_THREADS = SR_CW * 32;       // 352 consumer threads, 2 columns 
 constexpr int SR_WMAX = 2 * SR_THREADS;      // 704: widest column tile
 constexpr int SR_COLL = SR_THREADS;          // collector warp
 constexpr int SR_ALL = SR_THREADS + 32;      // 12 warps: 168 registers per thread
-constexpr int SR_NS = 4;                     // C ring slots (one panel each)
+constexpr int SR_NS = 6;                     // C ring slots (one panel each; 4 left ~6 % C-data waits at full HBM load)
 constexpr int SR_NSLOT = 16;                 // partial-sum slots in flight (>= 2 D)
 constexpr int SR_CPC = 40;                   // max CTAs per collector chunk (G <= 4 x 40)
 constexpr int SR_NR = 4;                     // per-warp row-sum buffers in flight (>= D + 1)
@@ -371,24 +371,23 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
     sr_wait(full + s, ph, s_abort);
     const char* st = ring + s * L::SLOT;
     double rs[NV];
-    if (has) {
+    {
+      // threads without columns (the last CTA's tail) compute on column pair 0 of the slot and
+      // contribute 0 to the row sums: no divergent zero-filling of the exps (their column sums
+      // are never written)
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(st);  // int64 shifts: low words at 2r
+      const int tc = has ? tcol : 0;
 #pragma unroll
       for (int r = 0; r < P; ++r) {
         const uint32_t ml = hdr[2 * r];
-        const double2 cc = *reinterpret_cast<const double2*>(st + L::HDR + r * L::ROWB + 16 * tcol);
+        const double2 cc = *reinterpret_cast<const double2*>(st + L::HDR + r * L::ROWB + 16 * tc);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           E[r][k][0] = texp(tb, fma(na[k], cc.x, nb[k][0]), ml);
           E[r][k][1] = texp(tb, fma(na[k], cc.y, nb[k][1]), ml);
-          rs[r * 2 + k] = E[r][k][0] + E[r][k][1];
+          rs[r * 2 + k] = has ? E[r][k][0] + E[r][k][1] : 0.0;
         }
       }
-    } else {
-#pragma unroll
-      for (int r = 0; r < P; ++r)
-#pragma unroll
-        for (int k = 0; k < 2; ++k) { E[r][k][0] = 0.0; E[r][k][1] = 0.0; rs[r * 2 + k] = 0.0; }
     }
     const int used = (int)s;
     if (++s == SR_NS) { s = 0; ph ^= 1; }

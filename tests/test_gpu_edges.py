@@ -27,8 +27,10 @@ def test_tiny_and_boundary_sizes_track_oracle(n):
     it, conv, iters, traj, col = O.solve(O.DenseCost(Cm), r, c, O.params_tuned(0.0, tau_mu=0.05), eps=1e-12,
                                           max_iter=60)
     assert sol.iterations == iters and sol.converged == conv     # n = 1 converges at the first log point
-    assert rel_err(sol.state.mu.delta, it.delta) <= 1e-10
-    assert rel_err(sol.state.weights.b, it.b) <= 1e-10
+    # delta lives in [-beta, beta] and b is O(a): compare on those scales (at n = 1 the reference's
+    # delta is exactly 0 while the device's is the rounding of 1 - sum_i p_ij, ~1e-16)
+    assert np.max(np.abs(sol.state.mu.delta - it.delta)) <= 1e-10 * max(1.0, np.max(np.abs(it.delta)))
+    assert np.max(np.abs(sol.state.weights.b - it.b)) <= 1e-10 * max(1.0, np.max(np.abs(it.b)))
     assert abs(sol.final.primal - traj[-1][1]) <= 1e-9 * max(1.0, abs(traj[-1][1]))
 
 
