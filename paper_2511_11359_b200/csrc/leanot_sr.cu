@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
     // every CTA computes bitwise the same S.
     // Generation tags: a value of parity `par` carries sign bit `par`; the raw doubles are
     // summed as they are (for par = 1 every term is negated, so S = -sum exactly) and a load
-    // is stale if any value's sign bit differs (OR of bits ^ parbits).
+    // is stale if any value's sign bit differs (OR of high words ^ parity bit).
     // The loads are direct relaxed loads, all in flight at once (LSU path: they do not queue
     // behind the C-tile bulk copies in the SM's TMA unit), and software-pipelined: panel
     // q + 1's loads are issued before panel q's S are finalized, so the L2 round trip
@@ -251,15 +251,17 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
       int rounds = 0;
       while (true) {
         a0 = a1 = c0 = c1 = 0.0;
-        unsigned long long bad = 0;
+        // sign bits only: one 3-input LOP per value on the high words
+        const unsigned p32 = (unsigned)(parbits >> 32);
+        unsigned bad = 0;
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj)
           if (jj < njj && 8 * jj + cl < G) {
-            bad |= ((unsigned long long)__double_as_longlong(y[jj].x) ^ parbits) |
-                   ((unsigned long long)__double_as_longlong(y[jj].y) ^ parbits);
+            bad |= ((unsigned)__double2hiint(y[jj].x) ^ p32);
+            bad |= ((unsigned)__double2hiint(y[jj].y) ^ p32);
             if (jj & 1) { c0 += y[jj].x; c1 += y[jj].y; } else { a0 += y[jj].x; a1 += y[jj].y; }
           }
-        if (!__any_sync(0xffffffffu, bad >> 63) || dead) break;
+        if (!__any_sync(0xffffffffu, bad >> 31) || dead) break;
         // some CTA had not published panel q when the loads ran: poll again
         ++rounds;
         const uint64_t el = sr_now() - t0;
