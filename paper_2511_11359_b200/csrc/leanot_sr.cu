@@ -43,25 +43,31 @@ constexpr int SR_CW = 11;                    // consumer warps
 constexpr int SR_THREADS = SR_CW * 32;       // 352 consumer threads, 2 columns each
 constexpr int SR_WMAX = 2 * SR_THREADS;      // 704: widest column tile
 constexpr int SR_COLL = SR_THREADS;          // collector warp
-constexpr int SR_ALL = SR_THREADS + 32;      // 12 warps: 168 registers per thread
 constexpr int SR_NS = 6;                     // C ring slots (one panel each; 4 left ~6 % C-data waits at full HBM load)
 constexpr int SR_NSLOT = 16;                 // partial-sum slots in flight (>= 2 D)
 constexpr int SR_CPC = 40;                   // max CTAs per collector chunk (G <= 4 x 40)
-constexpr int SR_NR = 4;                     // per-warp row-sum buffers in flight (>= D + 1)
+constexpr int SR_NR = 8;                     // per-warp row-sum buffers in flight (>= D + 1)
 constexpr uint64_t SR_TIMEOUT_NS = 4000000000ull;
+constexpr int SR_CNB = 8;                    // async collector (row groups): partial-sum buffers in smem
+#ifndef LEANOT_SR_LEAD
+#define LEANOT_SR_LEAD 3
+#endif
+constexpr int SR_LEAD = LEANOT_SR_LEAD;      // async collector: panels whose loads are in flight (< D - 1: issued after their publication)
 
-template <int P>
+template <int P, int NPR>
 struct SrLayout {
   static constexpr int NV = 2 * P;                      // (row, set) partials per panel
-  static constexpr int ROWB = SR_WMAX * 8;              // bytes per staged row
+  static constexpr int ROWB = NPR * SR_WMAX * 8;        // bytes per staged row
   static constexpr int HDR = 64;                        // shift values of the panel (P <= 8)
   static constexpr int SLOT = HDR + P * ROWB;
   static constexpr int RING = TAB_BYTES;                // ring after the exp table
   static constexpr int RED = RING + SR_NS * SLOT;       // [SR_NR][CW][NV] doubles
   static constexpr int WB = RED + SR_NR * SR_CW * NV * 8;  // [D][NV] doubles + [D][NV + 1] ints (<= 8 D)
   static constexpr int BAR = WB + 8 * (NV * 8 + (NV + 1) * 4 + 8);  // mbarriers (up to 8 D slots)
-  static constexpr int SMEM = BAR + 8 * (2 * SR_NS + 16) + 16;
-  static_assert(P <= 4 && (32 % NV) == 0, "SR panel shape (collector buffers hold 2P <= 8 values per CTA)");
+  static constexpr int CB = BAR + 8 * (2 * SR_NS + 16) + 16;   // async collector: [SR_CNB][K NV] doubles + SR_CNB mbarriers
+  static constexpr int SMEM = CB;
+  static constexpr int SMEM_ACOL = CB + SR_CNB * (4 * SR_CPC / 2) * NV * 8 + SR_CNB * 8;
+  static_assert(P <= 4 && (32 % NV) == 0 && P * NPR <= 4, "SR panel shape (collector buffers hold 2P <= 8 values per CTA)");
 };
 
 struct SrArgs {
@@ -76,10 +82,12 @@ struct SrArgs {
   double* coef;           // 2 x nr x 4 (written only by the fixup)
   int32_t* flags;         // [count, -, (k, li)...]
   double* col;            // 2 x n
+  double* gcol;           // NG > 1: NG x 2 x n column sums per row group (reduced in group order after the launch)
   unsigned long long* part;  // SR_NSLOT x G x NV tagged partials (0xff-filled before the launch)
   int32_t* err;
   int64_t W;              // column tile width (even)
   unsigned long long* trace;  // debug (null in production): per-panel timestamps of CTAs 0 and G-1
+  int dbg_nowait;         // debug timing only (LEANOT_SR_DBG_NOWAIT=1): consumers do not wait for g, no collector
 };
 
 __device__ __forceinline__ uint64_t sr_now() {
@@ -167,10 +175,49 @@ __device__ __forceinline__ double warp_transpose_sum(double (&x)[NV], int lane) 
   }
 }
 
-template <int P, int D, bool TRACE>
-__global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
-  using L = SrLayout<P>;
+
+// ---- TMEM parking of the exps (TM variant) ----
+// A consumer warp may touch only its lane quarter of TMEM (lanes 32 (warp % 4) ..); the
+// 32x32b shape gives each thread one lane, so a thread parks its 16 doubles of a panel as 32
+// consecutive 32-bit columns of its own lane.
+#define SR_R32(a) "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), \
+  "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]), "r"(a[15]), "r"(a[16]), \
+  "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]), "r"(a[22]), "r"(a[23]), "r"(a[24]), "r"(a[25]), \
+  "r"(a[26]), "r"(a[27]), "r"(a[28]), "r"(a[29]), "r"(a[30]), "r"(a[31])
+#define SR_W32(a) "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7]), \
+  "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]), "=r"(a[14]), "=r"(a[15]), \
+  "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]), "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), \
+  "=r"(a[24]), "=r"(a[25]), "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]), "=r"(a[31])
+#define SR_RW32(a) "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]), \
+  "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]), "+r"(a[15]), \
+  "+r"(a[16]), "+r"(a[17]), "+r"(a[18]), "+r"(a[19]), "+r"(a[20]), "+r"(a[21]), "+r"(a[22]), "+r"(a[23]), \
+  "+r"(a[24]), "+r"(a[25]), "+r"(a[26]), "+r"(a[27]), "+r"(a[28]), "+r"(a[29]), "+r"(a[30]), "+r"(a[31])
+
+__device__ __forceinline__ void sr_tm_st(uint32_t ta, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(ta), SR_R32(v) : "memory");
+}
+__device__ __forceinline__ void sr_tm_ld(uint32_t ta, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : SR_W32(v) : "r"(ta) : "memory");
+}
+// wait for this thread's TMEM loads; the loaded registers are tied to the wait so no use of
+// them can be scheduled above it
+__device__ __forceinline__ void sr_tm_wait_ld(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : SR_RW32(v) :: "memory");
+}
+__device__ __forceinline__ void sr_tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int P, int D, bool TRACE, bool TM, int NG, int NPR, bool ACOL>
+__global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrArgs F) {
+  using L = SrLayout<P, NPR>;
   constexpr int NV = L::NV;
+  constexpr int NE = P * NPR * 4;   // exps per thread and panel (rows x pairs x sets x 2 columns)
+  static_assert(!TM || NE == 16, "TMEM slot = 32 columns");
   extern __shared__ __align__(128) char smem[];
   char* ring = smem + L::RING;
   double* red = reinterpret_cast<double*>(smem + L::RED);
@@ -181,7 +228,10 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
   uint64_t* wfree = wready + D;
   volatile int* s_abort = reinterpret_cast<volatile int*>(wfree + D);
   int* s_cnt = reinterpret_cast<int*>(wfree + D + 1);               // [SR_NR] warps done with a panel
-  static_assert(SR_NS + 2 * D + 1 + SR_NR / 2 <= 2 * SR_NS + 16 && SR_NR >= D + 1, "SR barriers");
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cnt + SR_NR);     // TMEM base address (TM)
+  static_assert(SR_NS + 2 * D + 1 + SR_NR / 2 + 1 <= 2 * SR_NS + 16 && SR_NR >= D + 1 && 2 * D <= SR_NSLOT, "SR slots");
+  // TM: 3 consumer warps share a lane quarter, each parks D panels x 32 columns
+  static_assert(!TM || 3 * 32 * D <= 512, "TMEM slots");
   load_table(reinterpret_cast<double*>(smem));
   if (threadIdx.x == 0) {
     for (int s = 0; s < SR_NS; ++s) mbar_init(full + s, 1);
@@ -190,79 +240,122 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
     for (int i = 0; i < SR_NR; ++i) s_cnt[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (TM && threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = TM ? *reinterpret_cast<volatile uint32_t*>(s_tmem) : 0u;
 
   const CostView& cv = F.cost;
   const int64_t n = cv.n, nr = F.i1 - F.i0;
-  const int64_t npan = (nr + P - 1) / P;
+  const int64_t npan = (nr + P - 1) / P;                 // panels of the sweep
   const int G = gridDim.x, c = blockIdx.x;
-  const int64_t j0 = (int64_t)c * F.W, j1 = j0 + F.W < n ? j0 + F.W : n;
+  const int K = G / NG, grp = c / K, kc = c - grp * K;  // row group of this CTA and its rank in it
+  // group grp takes panels q = t NG + grp, t = 0 .. npl - 1
+  const int npl = (int)(npan > grp ? (npan - grp + NG - 1) / NG : 0);
+  const int64_t j0 = (int64_t)kc * F.W, j1 = j0 + F.W < n ? j0 + F.W : n;
   const uint32_t wbytes = j0 < j1 ? (uint32_t)((j1 - j0) * 8) : 0u;
   const int lane = threadIdx.x & 31;
-  // debug trace (clock64 of this SM), trace[q*8 + e]: 0 own partial published, 1 collector
-  // iteration start, 2 prefetched buffer ready, 3 re-polls done, 4 g posted, 5 consumer starts
-  // waiting for g, 6 consumer got g, 7 number of re-poll rounds
   unsigned long long* trace =
       TRACE && F.trace && (c == 0 || c == G - 1) ? F.trace + (c == 0 ? 0 : 8 * 4096) : nullptr;
-  if (!TRACE || npan > 4096) trace = nullptr;
+  if (!TRACE || npl > 4096) trace = nullptr;
 
+  if (threadIdx.x >= SR_COLL && F.dbg_nowait) return;
   if (threadIdx.x >= SR_COLL) {  // ------------------------- collector warp -------------------------
-    // Layout of a panel's partials: [CTA c][v = 2 r + k].  Lane l loads 16-byte pairs at
-    // doubles 2 l + 64 jj: values v0 = 2 (l % 4), v0 + 1 of CTA 8 jj + l / 4, so lanes l, l ^ 4,
-    // l ^ 8, l ^ 16 hold the same two values of different CTAs and three butterfly levels
-    // finish the sums.  The order (jj ascending per lane, then the butterfly) is fixed, so
-    // every CTA computes bitwise the same S.
+    // Layout of a panel's partials: [CTA c][v = 2 r + k], the group's K CTAs contiguous.  Lane
+    // l loads 16-byte pairs at doubles 2 l + 64 jj: values v0 = 2 (l % LPC), v0 + 1 of CTA
+    // CPL jj + l / LPC (LPC = NV / 2 lanes per CTA), so lanes l ^ LPC, l ^ 2 LPC, ... hold the
+    // same two values of other CTAs and butterfly levels o = LPC .. 16 finish the sums.  The
+    // order (jj ascending per lane, then the butterfly) is fixed, so every CTA of the group
+    // computes bitwise the same S.
     // Generation tags: a value of parity `par` carries sign bit `par`; the raw doubles are
     // summed as they are (for par = 1 every term is negated, so S = -sum exactly) and a load
-    // is stale if any value's sign bit differs (OR of high words ^ parity bit).
-    // The loads are direct relaxed loads, all in flight at once (LSU path: they do not queue
-    // behind the C-tile bulk copies in the SM's TMA unit), and software-pipelined: panel
-    // q + 1's loads are issued before panel q's S are finalized, so the L2 round trip
-    // overlaps the finalization.
-    static_assert(NV == 8, "collector layout assumes P = 4");
-    constexpr int NJ = (4 * SR_CPC * 8) / 64;              // 16-byte loads per lane covering G <= 160
-    const int cl = lane >> 2;                              // CTA offset within a group of 8
-    const int njj = (G + 7) / 8;
+    // is stale if any value's sign bit differs.
+    // The loads are direct relaxed loads, all in flight at once, and software-pipelined:
+    // panel t + 1's loads are issued before panel t's S are finalized.
+    constexpr int LPC = NV / 2, CPL = 32 / LPC;
+    constexpr int NJ = (4 * SR_CPC / NG * NV + 63) / 64;   // 16-byte loads per lane covering K <= 160 / NG
+    const int cl = lane / LPC;
+    const int njj = (K + CPL - 1) / CPL;
     bool dead = false;
     double2 y[NJ];
-    auto issue = [&](int64_t q) {
-      const double2* gp = reinterpret_cast<const double2*>(F.part + (q % SR_NSLOT) * G * NV) + lane;
+    auto issue = [&](int t) {
+      const double2* gp = reinterpret_cast<const double2*>(F.part + ((t % SR_NSLOT) * G + grp * K) * NV) + lane;
 #pragma unroll
       for (int jj = 0; jj < NJ; ++jj)
-        if (jj < njj && 8 * jj + cl < G) {
+        if (jj < njj && CPL * jj + cl < K) {
           unsigned long long u0, u1;
           asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(u0), "=l"(u1) : "l"(gp + 32 * jj));
           y[jj] = make_double2(__longlong_as_double((long long)u0), __longlong_as_double((long long)u1));
         }
     };
-    if (npan > 0) issue(0);
-    // lanes 0..3 finalize row r = lane of each panel: r_i prefetched one panel ahead
-    double rw_next = (lane < P && lane < nr) ? __ldg(F.rw + F.i0 + lane) : 0.0;
-    for (int64_t q = 0; q < npan; ++q) {
-      const unsigned long long parbits = (unsigned long long)((q / SR_NSLOT) & 1) << 63;
+    // ACOL: the group's partials of panel t arrive by cp.async (L2, 16 bytes per lane) in smem
+    // buffer t % SR_CNB, completion on that buffer's mbarrier (32 lane arrivals per issue);
+    // loads of the next SR_LEAD panels are in flight while panel t is finalized, so the
+    // collector is not limited to one L2 round trip per panel
+    static_assert(!ACOL || NG == 2, "async collector buffers are sized for two row groups");
+    constexpr int KNV = (4 * SR_CPC / 2) * NV;                 // buffer doubles (K <= 80)
+    double* cb = reinterpret_cast<double*>(smem + L::CB);
+    uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + L::CB + SR_CNB * KNV * 8);
+    uint32_t cph = 0;                                           // wait parity per buffer
+    auto aissue = [&](int t) {
+      const int bi = t % SR_CNB;
+      const char* src = reinterpret_cast<const char*>(F.part + ((t % SR_NSLOT) * G + grp * K) * NV);
+      const uint32_t dst = smem_u32(cb + bi * KNV);
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj)
+        if (jj < njj && CPL * jj + cl < K)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * (lane + 32 * jj)),
+                       "l"(src + 16 * (lane + 32 * jj)) : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(cbar + bi)) : "memory");
+    };
+    if (ACOL) {
+      if (lane == 0)
+        for (int i = 0; i < SR_CNB; ++i) mbar_init(cbar + i, 32);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      __syncwarp();
+      for (int u = 0; u < SR_LEAD && u < npl; ++u) aissue(u);
+    } else if (npl > 0) {
+      issue(0);
+    }
+    // lanes 0 .. P-1 finalize row r = lane of each panel: r_i prefetched one panel ahead
+    auto row_of = [&](int t) { return ((int64_t)t * NG + grp) * P + lane; };
+    double rw_next = (lane < P && npl > 0 && row_of(0) < nr) ? __ldg(F.rw + F.i0 + row_of(0)) : 0.0;
+    for (int t = 0; t < npl; ++t) {
+      const unsigned long long parbits = (unsigned long long)((t / SR_NSLOT) & 1) << 63;
       const double rw_q = rw_next;
-      if (q + 1 < npan && lane < P) {
-        const int64_t li1 = (q + 1) * P + lane;
+      if (t + 1 < npl && lane < P) {
+        const int64_t li1 = row_of(t + 1);
         rw_next = li1 < nr ? __ldg(F.rw + F.i0 + li1) : 0.0;
       }
-      if (TRACE && trace && lane == 0) trace[q * 8 + 1] = clock64();
+      if (TRACE && trace && lane == 0) trace[t * 8 + 1] = clock64();
       double a0, a1, c0, c1;   // (v0, v1) x (even jj, odd jj)
       const uint64_t t0 = sr_now();
       int rounds = 0;
       while (true) {
+        if (ACOL) {   // wait for this panel's buffer, then read it
+          const int bi = t % SR_CNB;
+          sr_wait(cbar + bi, (cph >> bi) & 1u, s_abort);
+          cph ^= 1u << bi;
+          const double2* bp = reinterpret_cast<const double2*>(cb + bi * KNV) + lane;
+#pragma unroll
+          for (int jj = 0; jj < NJ; ++jj)
+            if (jj < njj && CPL * jj + cl < K) y[jj] = bp[32 * jj];
+        }
         a0 = a1 = c0 = c1 = 0.0;
-        // sign bits only: one 3-input LOP per value on the high words
         const unsigned p32 = (unsigned)(parbits >> 32);
         unsigned bad = 0;
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj)
-          if (jj < njj && 8 * jj + cl < G) {
+          if (jj < njj && CPL * jj + cl < K) {
             bad |= ((unsigned)__double2hiint(y[jj].x) ^ p32);
             bad |= ((unsigned)__double2hiint(y[jj].y) ^ p32);
             if (jj & 1) { c0 += y[jj].x; c1 += y[jj].y; } else { a0 += y[jj].x; a1 += y[jj].y; }
           }
         if (!__any_sync(0xffffffffu, bad >> 31) || dead) break;
-        // some CTA had not published panel q when the loads ran: poll again
         ++rounds;
         const uint64_t el = sr_now() - t0;
         if (__any_sync(0xffffffffu, el > SR_TIMEOUT_NS || (el > 1000000ull && *(volatile int32_t*)F.err != 0))) {
@@ -270,26 +363,36 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
           if (lane == 0) atomicExch(F.err, 1);
           break;
         }
-        issue(q);
+        if (ACOL) {
+          __syncwarp();
+          aissue(t);
+        } else {
+          issue(t);
+        }
       }
-      if (q + 1 < npan) issue(q + 1);   // next panel's round trip overlaps this finalization
-      if (TRACE && trace && lane == 0) { trace[q * 8 + 2] = clock64(); trace[q * 8 + 7] = rounds; }
+      if (ACOL) {
+        __syncwarp();   // every lane has read buffer t % SR_CNB before any reuse
+        if (t + SR_LEAD < npl) aissue(t + SR_LEAD);
+      } else if (t + 1 < npl) {
+        issue(t + 1);   // next panel's round trip overlaps this finalization
+      }
+      if (TRACE && trace && lane == 0) { trace[t * 8 + 2] = clock64(); trace[t * 8 + 7] = rounds; }
       double s0 = a0 + c0, s1 = a1 + c1;
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
+      for (int o = LPC; o < 32; o <<= 1) {
         s0 += __shfl_xor_sync(0xffffffffu, s0, o);
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       }
       if (parbits) { s0 = -s0; s1 = -s1; }
-      if (TRACE && trace && lane == 0) trace[q * 8 + 3] = clock64();
-      // lanes 0..3: row r = lane, S0 = S of the current weights, S1 = S of the midpoint weights
-      const int64_t li = q * P + lane;
+      if (TRACE && trace && lane == 0) trace[t * 8 + 3] = clock64();
+      // lanes 0..P-1: row r = lane, S0 = S of the current weights, S1 = S of the midpoint weights
+      const int64_t li = row_of(t);
       const bool valid = lane < P && li < nr;
       const bool ok0 = valid && sum_ok(s0) && !dead, ok1 = valid && sum_ok(s1) && !dead;
       // g = r_i / S: one correctly rounded reciprocal and a multiply (<= 1.5 ulp of the quotient)
       const double w0 = ok0 ? rw_q * __drcp_rn(s0) : 0.0, w1 = ok1 ? rw_q * __drcp_rn(s1) : 0.0;
-      const int ds = (int)(q % D);
-      if (q >= D) sr_wait(wfree + ds, (uint32_t)(((q / D) - 1) & 1), s_abort);
+      const int ds = t % D;
+      if (t >= D) sr_wait(wfree + ds, (uint32_t)(((t / D) - 1) & 1), s_abort);
       if (lane < P) {
         wbuf[ds * NV + 2 * lane] = w0;
         wbuf[ds * NV + 2 * lane + 1] = w1;
@@ -299,9 +402,9 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
       const bool all = __all_sync(0xffffffffu, lane >= P || (ok0 && ok1));
       if (lane == 0) okbuf[ds * (NV + 1) + NV] = all ? 1 : 0;
       __syncwarp();
-      if (TRACE && trace && lane == 0) trace[q * 8 + 4] = clock64();
+      if (TRACE && trace && lane == 0) trace[t * 8 + 4] = clock64();
       if (lane == 0) mbar_arrive(wready + ds);
-      if (valid && (int)(q % G) == c) {  // this CTA finalizes the panel's rows (off the consumers' path)
+      if (valid && t % K == kc) {  // one CTA of the group finalizes the panel's rows (off the consumers' path)
         const int64_t m = F.shift[li];
         F.S[li] = s0;
         F.S[nr + li] = s1;
@@ -323,25 +426,33 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
   const uint32_t tb = lane_tab_addr(smem);
   const int warp = threadIdx.x >> 5;
   // Column group of this warp.  Warp w issues on SMSP w % 4; the collector (warp 11) shares
-  // SMSP 3 with warps 3 and 7, so warp 7 takes the LAST column group, which is only partly
-  // filled when W < 704 (n = 1e5: 36 of 64 columns), leaving the collector issue slots.
+  // SMSP 3 with warps 3 and 7, so warp 7 takes the LAST column group, which is the least
+  // filled when W < NPR x 704, leaving the collector issue slots.
   const int cgrp = warp == 7 ? SR_CW - 1 : (warp == SR_CW - 1 ? 7 : warp);
   const int tcol = cgrp * 32 + lane;
-  const int64_t jt = 2 * tcol;                  // local column pair
-  const bool has = j0 + jt < j1;                // n and W even: pairs are whole
-  double na[2], nb[2][2], acc[2][2];
+  // column pair u of this thread: local columns jt[u], jt[u] + 1 (n and W even: pairs are whole)
+  int jt[NPR];
+  bool has[NPR];
+  double na[2], nb[2][NPR][2], acc[2][NPR][2];
+#pragma unroll
+  for (int u = 0; u < NPR; ++u) {
+    jt[u] = 2 * tcol + 2 * SR_THREADS * u;
+    has[u] = j0 + jt[u] < j1;
+  }
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     na[k] = -F.a[k];
-    nb[k][0] = has ? -__ldg(F.b[k] + j0 + jt) : 0.0;
-    nb[k][1] = has ? -__ldg(F.b[k] + j0 + jt + 1) : 0.0;
-    acc[k][0] = 0.0; acc[k][1] = 0.0;
+#pragma unroll
+    for (int u = 0; u < NPR; ++u) {
+      nb[k][u][0] = has[u] ? -__ldg(F.b[k] + j0 + jt[u]) : 0.0;
+      nb[k][u][1] = has[u] ? -__ldg(F.b[k] + j0 + jt[u] + 1) : 0.0;
+      acc[k][u][0] = 0.0; acc[k][u][1] = 0.0;
+    }
   }
-  double e[D][P][2][2];
   uint32_t s = 0, ph = 0;
-  // thread 0: fill ring slot `slot` with panel p (row shifts + the C tile rows)
-  auto refill = [&](int p, int slot) {
-    const int64_t li0 = p * P;
+  // thread 0: fill ring slot `slot` with local panel t (row shifts + the C tile rows)
+  auto refill = [&](int t, int slot) {
+    const int64_t li0 = ((int64_t)t * NG + grp) * P;
     const int rows = (int)(nr - li0 < P ? nr - li0 : P);
     char* dst = ring + slot * L::SLOT;
     uint64_t* bar = full + slot;
@@ -363,13 +474,12 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
     }
   };
   if (threadIdx.x == 0)
-    for (int q = 0; q < SR_NS && q < npan; ++q) refill(q, q);
+    for (int q = 0; q < SR_NS && q < npl; ++q) refill(q, q);
   // running panel bookkeeping (32-bit, no divisions in the loop): reduction buffer pr = p % NR,
   // partial-sum slot ps = p % NSLOT with generation parity pp
   int pr = 0, ps = 0;
   unsigned long long pp = 0;
-  const int npan32 = (int)npan;
-  auto compute = [&](int p, double (&E)[P][2][2]) {
+  auto compute = [&](int p, double (&E)[P][NPR][2][2]) {
     sr_wait(full + s, ph, s_abort);
     const char* st = ring + s * L::SLOT;
     double rs[NV];
@@ -378,16 +488,21 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
       // contribute 0 to the row sums: no divergent zero-filling of the exps (their column sums
       // are never written)
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(st);  // int64 shifts: low words at 2r
-      const int tc = has ? tcol : 0;
 #pragma unroll
       for (int r = 0; r < P; ++r) {
         const uint32_t ml = hdr[2 * r];
-        const double2 cc = *reinterpret_cast<const double2*>(st + L::HDR + r * L::ROWB + 16 * tc);
+        rs[r * 2] = 0.0;
+        rs[r * 2 + 1] = 0.0;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          E[r][k][0] = texp(tb, fma(na[k], cc.x, nb[k][0]), ml);
-          E[r][k][1] = texp(tb, fma(na[k], cc.y, nb[k][1]), ml);
-          rs[r * 2 + k] = has ? E[r][k][0] + E[r][k][1] : 0.0;
+        for (int u = 0; u < NPR; ++u) {
+          const int tc = has[u] ? jt[u] : 0;
+          const double2 cc = *reinterpret_cast<const double2*>(st + L::HDR + r * L::ROWB + 8 * tc);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            E[r][u][k][0] = texp(tb, fma(na[k], cc.x, nb[k][u][0]), ml);
+            E[r][u][k][1] = texp(tb, fma(na[k], cc.y, nb[k][u][1]), ml);
+            rs[r * 2 + k] += has[u] ? E[r][u][k][0] + E[r][u][k][1] : 0.0;
+          }
         }
       }
     }
@@ -411,7 +526,7 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
       __threadfence_block();
       if (lane == 0) {
         s_cnt[pr] = 0;   // reused NR panels later, after this CTA's partial of p + 1 is out
-        if (p + SR_NS < npan32) refill(p + SR_NS, used);
+        if (p + SR_NS < npl) refill(p + SR_NS, used);
       }
       if (lane < NV) {
         const volatile double* vb = rb;
@@ -427,9 +542,9 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
     if (++ps == SR_NSLOT) { ps = 0; pp ^= 1ull << 63; }
   };
   // fold panel q (exps E, slot ds = q % D, wready parity wpar) into the column sums
-  auto accumulate = [&](int q, const double (&E)[P][2][2], int ds, uint32_t wpar) {
+  auto accumulate = [&](int q, const double (&E)[P][NPR][2][2], int ds, uint32_t wpar) {
     if (TRACE && trace && threadIdx.x == 0) trace[q * 8 + 5] = clock64();
-    sr_wait(wready + ds, wpar, s_abort);
+    if (!F.dbg_nowait) sr_wait(wready + ds, wpar, s_abort);
     if (TRACE && trace && threadIdx.x == 0) trace[q * 8 + 6] = clock64();
     const double* wq = wbuf + ds * NV;
     const int* oq = okbuf + ds * (NV + 1);
@@ -439,8 +554,11 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const double g = wq[r * 2 + k];
-          acc[k][0] = fma(g, E[r][k][0], acc[k][0]);
-          acc[k][1] = fma(g, E[r][k][1], acc[k][1]);
+#pragma unroll
+          for (int u = 0; u < NPR; ++u) {
+            acc[k][u][0] = fma(g, E[r][u][k][0], acc[k][u][0]);
+            acc[k][u][1] = fma(g, E[r][u][k][1], acc[k][u][1]);
+          }
         }
     } else {
 #pragma unroll
@@ -449,47 +567,97 @@ __global__ void __launch_bounds__(SR_ALL, 1) sr_sweep_kernel(const SrArgs F) {
         for (int k = 0; k < 2; ++k)
           if (oq[r * 2 + k]) {
             const double g = wq[r * 2 + k];
-            acc[k][0] = fma(g, E[r][k][0], acc[k][0]);
-            acc[k][1] = fma(g, E[r][k][1], acc[k][1]);
+#pragma unroll
+            for (int u = 0; u < NPR; ++u) {
+              acc[k][u][0] = fma(g, E[r][u][k][0], acc[k][u][0]);
+              acc[k][u][1] = fma(g, E[r][u][k][1], acc[k][u][1]);
+            }
           }
     }
     release(wfree + ds);
   };
-  // p0 steps by D, so panel p = p0 + u keeps its exps in e[u] and panel q = p - (D - 1) is in
-  // e[(u + 1) % D] with wready slot (u + 1) % D; its use index q / D is p0 / D for u = D - 1
-  // and p0 / D - 1 otherwise (phase bit wph tracks p0 / D)
-  uint32_t wph = 0;
-  for (int p0 = 0; p0 < npan32 + D - 1; p0 += D, wph ^= 1) {
-#pragma unroll
-    for (int u = 0; u < D; ++u) {
-      const int p = p0 + u;
-      if (p < npan32) compute(p, e[u]);
+  if constexpr (TM) {
+    // exps parked in TMEM: panel p is computed in registers, stored to slot p % D, and
+    // reloaded for the fold D - 1 panels later (the load is issued before the next compute)
+    const uint32_t tw = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 32 * D);
+    double E[P][NPR][2][2];
+    uint32_t Fv[32];
+    for (int p = 0; p < npl + D - 1; ++p) {
       const int q = p - (D - 1);
-      if (q >= 0 && q < npan32) accumulate(q, e[(u + 1) % D], (u + 1) % D, u == D - 1 ? wph : wph ^ 1);
+      sr_tm_wait_st();   // the previous panel's store (q <= p - 2 was stored before it)
+      if (q >= 0) sr_tm_ld(tw + 32 * (q % D), Fv);
+      if (p < npl) {
+        compute(p, E);
+        uint32_t ev[32];
+        const double* Ef = &E[0][0][0][0];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          ev[2 * i] = (uint32_t)__double2loint(Ef[i]);
+          ev[2 * i + 1] = (uint32_t)__double2hiint(Ef[i]);
+        }
+        sr_tm_st(tw + 32 * (p % D), ev);
+      }
+      if (q >= 0) {
+        sr_tm_wait_ld(Fv);
+        double Eq[P][NPR][2][2];
+        double* Ef = &Eq[0][0][0][0];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Ef[i] = __hiloint2double((int)Fv[2 * i + 1], (int)Fv[2 * i]);
+        accumulate(q, Eq, q % D, (uint32_t)((q / D) & 1));
+      }
+    }
+  } else {
+    double e[D][P][NPR][2][2];
+    // p0 steps by D, so panel p = p0 + u keeps its exps in e[u] and panel q = p - (D - 1) is in
+    // e[(u + 1) % D] with wready slot (u + 1) % D; its use index q / D is p0 / D for u = D - 1
+    // and p0 / D - 1 otherwise (phase bit wph tracks p0 / D)
+    uint32_t wph = 0;
+    for (int p0 = 0; p0 < npl + D - 1; p0 += D, wph ^= 1) {
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        const int p = p0 + u;
+        if (p < npl) compute(p, e[u]);
+        const int q = p - (D - 1);
+        if (q >= 0 && q < npl) accumulate(q, e[(u + 1) % D], (u + 1) % D, u == D - 1 ? wph : wph ^ 1);
+      }
     }
   }
-  if (has) {
+  // column sums of this group's rows: directly into col (one group) or into the group's slab
+  double* out = NG == 1 ? F.col : F.gcol + (int64_t)grp * 2 * n;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      F.col[k * n + j0 + jt] = acc[k][0];
-      F.col[k * n + j0 + jt + 1] = acc[k][1];
+  for (int u = 0; u < NPR; ++u)
+    if (has[u]) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        out[k * n + j0 + jt[u]] = acc[k][u][0];
+        out[k * n + j0 + jt[u] + 1] = acc[k][u][1];
+      }
     }
+  if (TM) {   // consumers only (the collector has returned): free TMEM after every warp's last load
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(SR_THREADS) : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }
   if (*s_abort && threadIdx.x == 0) atomicExch(F.err, 2);
 }
 
-#ifndef LEANOT_SR_P
-#define LEANOT_SR_P 4
-#endif
-#ifndef LEANOT_SR_D
-#define LEANOT_SR_D 3
-#endif
+// Variants (LEANOT_SR_VAR): 'g' (default) row groups: NG = 2 groups of G / 2 CTAs, each
+// group sweeps every other panel of P = 2 rows over column tiles of W <= 1408 (2 column pairs
+// per thread), exps parked in TMEM for D = 5 panels, the two groups' column sums reduced in
+// group order after the launch; 't': one group, P = 4 rows, 1 pair per thread, TMEM (D = 5);
+// 'r': one group, exps in registers (D = 3).
+static char sr_variant() {
+  static char v = 0;
+  if (!v) {
+    const char* e = getenv("LEANOT_SR_VAR");
+    v = (e && (e[0] == 't' || e[0] == 'r' || e[0] == 'h')) ? e[0] : 'g';
+  }
+  return v;
+}
 
-// LEANOT_SR=1 makes the single-read sweep the default for eligible plans.  It is opt-in: at
-// n = 1e5 it measures 40.3 ms per iteration against 36.8 ms for the two-pass sweep
-// (profiles/r02_single_read.md: the 148-way exchange of row partials through L2 takes
-// ~1-1.5 us under full HBM load, more than the ~12 rows of exps the register file can hold
-// while it is in flight; engine.sweep(single_read=True) / LEANOT_SWEEP_SINGLE_READ force it)
+// LEANOT_SR=1 makes the single-read sweep the default for eligible plans (engine.sweep(
+// single_read=True) / LEANOT_SWEEP_SINGLE_READ force it).
 static bool sr_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -512,58 +680,61 @@ static int64_t sr_min_n() {
 // debug trace buffer (leanot_debug_sr_trace): 2 x 8 x 4096 u64 stamps, null in production
 static unsigned long long* g_sr_trace = nullptr;
 
-// workspace doubles the single-read sweep carves from plan.slab
-static int64_t sr_ws_doubles(int G) { return (int64_t)SR_NSLOT * G * 2 * LEANOT_SR_P + 2; }
+// partial-sum slots + error flag the single-read sweep carves from plan.slab (NV = 8 covers
+// every variant: 2 P <= 8)
+static int64_t sr_ws_doubles(int G) { return (int64_t)SR_NSLOT * G * 8 + 2; }
 
-// Launch the single-read sweep for a plain DXG iteration if the plan qualifies (stored
-// cost on the TMA path, n >= sr_min_n(), column tile <= 704, slab large enough);
-// LEANOT_EINVAL: the caller runs the two-pass sweep.
-static int try_sr_sweep(const leanot_dxg_plan_t& P, cudaStream_t st, bool force = false) {
-  constexpr int SP = LEANOT_SR_P, SD = LEANOT_SR_D;
-  using Lay = SrLayout<SP>;
-  const CostView cv = make_view(P.cost);
-  if (!tma_ok(cv) || (!force && (!sr_enabled() || P.n < sr_min_n()))) return LEANOT_EINVAL;
+template <int P, int D, bool TM, int NG, int NPR, bool ACOL>
+static int launch_sr_variant(const leanot_dxg_plan_t& Pl, const CostView& cv, cudaStream_t st) {
+  using Lay = SrLayout<P, NPR>;
+  constexpr int SMEM = ACOL ? Lay::SMEM_ACOL : Lay::SMEM;
   const int G = num_sms();
-  if (G > 4 * SR_CPC) return LEANOT_EINVAL;
-  const int64_t W = (((P.n + G - 1) / G) + 1) & ~int64_t(1);
-  if (W > SR_WMAX) return LEANOT_EINVAL;
-  if (sr_ws_doubles(G) > (int64_t)P.splits * 2 * P.n) return LEANOT_EINVAL;
-  auto kern = g_sr_trace ? sr_sweep_kernel<SP, SD, true> : sr_sweep_kernel<SP, SD, false>;
+  if (G % NG != 0 || G / NG > 4 * SR_CPC / NG) return LEANOT_EINVAL;
+  const int K = G / NG;
+  const int64_t W = (((Pl.n + K - 1) / K) + 1) & ~int64_t(1);
+  if (W > NPR * SR_WMAX) return LEANOT_EINVAL;
+  const int64_t gcol_off = (sr_ws_doubles(G) + 15) & ~int64_t(15);
+  const int64_t need = NG > 1 ? gcol_off + (int64_t)NG * 2 * Pl.n : sr_ws_doubles(G);
+  if (need > (int64_t)Pl.splits * 2 * Pl.n) return LEANOT_EINVAL;
+  auto kern = g_sr_trace ? sr_sweep_kernel<P, D, true, TM, NG, NPR, ACOL> : sr_sweep_kernel<P, D, false, TM, NG, NPR, ACOL>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(sr_sweep_kernel<SP, SD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Lay::SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(sr_sweep_kernel<SP, SD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Lay::SMEM) != cudaSuccess)
-      return LEANOT_EINVAL;
+    for (auto kk : {sr_sweep_kernel<P, D, true, TM, NG, NPR, ACOL>, sr_sweep_kernel<P, D, false, TM, NG, NPR, ACOL>})
+      if (cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+        return LEANOT_EINVAL;
     if (cudaFuncSetAttribute(fused_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess)
       return LEANOT_EINVAL;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SR_ALL, Lay::SMEM) != cudaSuccess || occ < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SR_THREADS + 32, SMEM) != cudaSuccess || occ < 1)
       return LEANOT_EINVAL;
     attr = true;
   }
   SrArgs F;
   memset(&F, 0, sizeof(F));
   F.cost = cv;
-  F.i0 = P.row0; F.i1 = P.row1;
-  F.a = P.scal;
-  F.b[0] = P.b; F.b[1] = P.b_bar;
-  F.rw = P.r;
-  F.shift = P.shift; F.m_used = P.m; F.S = P.S; F.coef = P.coef;
-  F.flags = P.flags; F.col = P.col;
-  F.part = reinterpret_cast<unsigned long long*>(P.slab);
-  F.err = reinterpret_cast<int32_t*>(P.slab + sr_ws_doubles(G) - 2);
+  F.i0 = Pl.row0; F.i1 = Pl.row1;
+  F.a = Pl.scal;
+  F.b[0] = Pl.b; F.b[1] = Pl.b_bar;
+  F.rw = Pl.r;
+  F.shift = Pl.shift; F.m_used = Pl.m; F.S = Pl.S; F.coef = Pl.coef;
+  F.flags = Pl.flags; F.col = Pl.col;
+  F.gcol = NG > 1 ? Pl.slab + gcol_off : nullptr;
+  F.part = reinterpret_cast<unsigned long long*>(Pl.slab);
+  F.err = reinterpret_cast<int32_t*>(Pl.slab + sr_ws_doubles(G) - 2);
   F.W = W;
   F.trace = g_sr_trace;
+  {
+    const char* e = getenv("LEANOT_SR_DBG_NOWAIT");
+    F.dbg_nowait = (e && e[0] == '1') ? 1 : 0;
+  }
   // generation-0 slots must read as "not ready": sign bit set (0xff bytes), error flag 0
   cudaMemsetAsync(F.part, 0xff, (size_t)(sr_ws_doubles(G) - 2) * 8, st);
   cudaMemsetAsync(F.err, 0, 16, st);
   cudaLaunchConfig_t lc;
   memset(&lc, 0, sizeof(lc));
   lc.gridDim = dim3(G);
-  lc.blockDim = dim3(SR_ALL);
-  lc.dynamicSmemBytes = Lay::SMEM;
+  lc.blockDim = dim3(SR_THREADS + 32);
+  lc.dynamicSmemBytes = SMEM;
   lc.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeCooperative;
@@ -575,13 +746,31 @@ static int try_sr_sweep(const leanot_dxg_plan_t& P, cudaStream_t st, bool force 
     set_error("single-read sweep launch: %s", cudaGetErrorString(e));
     return LEANOT_ECUDA;
   }
+  // row groups: their column sums added in group order (deterministic)
+  if (NG > 1) LEANOT_TRY(launch_slab_reduce(F.gcol, NG, 2, Pl.n, Pl.col, st));
   // flagged rows: exact recompute + their column contributions (FusedArgs view of the same buffers)
   FusedArgs X;
   memset(&X, 0, sizeof(X));
-  X.cost = cv; X.i0 = P.row0; X.i1 = P.row1; X.a = P.scal; X.b[0] = P.b; X.b[1] = P.b_bar; X.rw = P.r;
-  X.shift = P.shift; X.m_used = P.m; X.S = P.S; X.coef = P.coef; X.flags = P.flags; X.col = P.col;
+  X.cost = cv; X.i0 = Pl.row0; X.i1 = Pl.row1; X.a = Pl.scal; X.b[0] = Pl.b; X.b[1] = Pl.b_bar; X.rw = Pl.r;
+  X.shift = Pl.shift; X.m_used = Pl.m; X.S = Pl.S; X.coef = Pl.coef; X.flags = Pl.flags; X.col = Pl.col;
   fused_fix_kernel<<<1, 1024, TAB_BYTES, st>>>(X);
   return LEANOT_OK;
+}
+
+// Launch the single-read sweep for a plain DXG iteration if the plan qualifies (stored
+// cost on the TMA path, n >= sr_min_n(), column tile within the variant's width, slab large
+// enough); LEANOT_EINVAL: the caller runs the two-pass sweep.
+static int try_sr_sweep(const leanot_dxg_plan_t& P, cudaStream_t st, bool force = false) {
+  const CostView cv = make_view(P.cost);
+  if (!tma_ok(cv) || (!force && (!sr_enabled() || P.n < sr_min_n()))) return LEANOT_EINVAL;
+  const char v = sr_variant();
+  if (v == 'g' || v == 'h') {
+    const int rc = v == 'g' ? launch_sr_variant<2, 5, true, 2, 2, true>(P, cv, st)
+                            : launch_sr_variant<2, 5, true, 2, 2, false>(P, cv, st);
+    if (rc != LEANOT_EINVAL) return rc;   // plans outside the grouped shape take the one-group form
+  }
+  if (v == 'r') return launch_sr_variant<4, 3, false, 1, 1, false>(P, cv, st);
+  return launch_sr_variant<4, 5, true, 1, 1, false>(P, cv, st);
 }
 
 }  // namespace leanot
