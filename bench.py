@@ -319,8 +319,9 @@ def run_b200(args):
                     "counts the second read as work; the iteration fraction above does not"},
         "limiter": "the two-pass sweep reads C twice and evaluates 4 exps per element; the board "
                    "sits at its 1 kW cap (sw_power_cap) running ~8 FP64 + 5 other instructions per exp "
-                   "(profiles/r01_power.md); the single-read kernel (csrc/leanot_sr.cu, opt-in) is "
-                   "exchange-latency bound (profiles/r02_single_read.md)",
+                   "(profiles/r01_power.md); the single-read kernel (csrc/leanot_sr.cu, opt-in, 2 exps per "
+                   "element) is bound by its consumer instruction stream (32 ms with the exchange and the "
+                   "C copies disabled; profiles/r02/sr_instr_mix.md)",
         "sweep": {"what": "pass A + pass B (one DXG iteration's n^2 work)", "seconds": t_sweep,
                   "hbm_frac_vs_one_read": bytes_alg / t_sweep / 1e9 / peak,
                   "fp64_instr_per_s": fp64_per_elem * n * nr / t_sweep,

@@ -35,13 +35,21 @@
 // shifts (from the midpoint set, as finalize_row), the fixup list.  Deterministic: fixed
 // reduction orders everywhere, no floating-point atomics.  Every spin loop has a 4 s
 // timeout that sets an error flag and drains the launch (never expected).
+// Variants (template parameters, LEANOT_SR_VAR): the default 'g' splits the CTAs into NG = 2
+// row groups of G / 2 (each group sweeps every other panel over column tiles twice as wide,
+// P = 2 rows x 2 column pairs per thread, so a row's sum is exchanged among 74 CTAs, not 148),
+// parks the exps of the panels in flight in TMEM (tcgen05.st/ld, D = 5 panels) and lets the
+// collector read the group's partials by cp.async into shared-memory buffers with several
+// panels in flight; the groups' column sums are added in group order after the launch.
+// Measured: all variants take ~37 ms per n = 1e5 iteration and 32 ms even
+// with the exchange and the C copies disabled (LEANOT_SR_DBG_NOWAIT, debug timing only):
+// the consumer instruction stream, not the exchange, is what binds.
 // Included by leanot_lib.cu after leanot_fused.cu (mbarrier / bulk-copy helpers).
 
 namespace leanot {
 
 constexpr int SR_CW = 11;                    // consumer warps
 constexpr int SR_THREADS = SR_CW * 32;       // 352 consumer threads, 2 columns each
-constexpr int SR_WMAX = 2 * SR_THREADS;      // 704: widest column tile
 constexpr int SR_COLL = SR_THREADS;          // collector warp
 constexpr int SR_NS = 6;                     // C ring slots (one panel each; 4 left ~6 % C-data waits at full HBM load)
 constexpr int SR_NSLOT = 16;                 // partial-sum slots in flight (>= 2 D)
@@ -54,20 +62,20 @@ constexpr int SR_CNB = 8;                    // async collector (row groups): pa
 #endif
 constexpr int SR_LEAD = LEANOT_SR_LEAD;      // async collector: panels whose loads are in flight (< D - 1: issued after their publication)
 
-template <int P, int NPR>
+template <int P, int NPR, int CW = SR_CW>
 struct SrLayout {
   static constexpr int NV = 2 * P;                      // (row, set) partials per panel
-  static constexpr int ROWB = NPR * SR_WMAX * 8;        // bytes per staged row
+  static constexpr int ROWB = NPR * 2 * CW * 32 * 8;    // bytes per staged row
   static constexpr int HDR = 64;                        // shift values of the panel (P <= 8)
   static constexpr int SLOT = HDR + P * ROWB;
   static constexpr int RING = TAB_BYTES;                // ring after the exp table
   static constexpr int RED = RING + SR_NS * SLOT;       // [SR_NR][CW][NV] doubles
-  static constexpr int WB = RED + SR_NR * SR_CW * NV * 8;  // [D][NV] doubles + [D][NV + 1] ints (<= 8 D)
+  static constexpr int WB = RED + SR_NR * CW * NV * 8;  // [D][NV] doubles + [D][NV + 1] ints (<= 8 D)
   static constexpr int BAR = WB + 8 * (NV * 8 + (NV + 1) * 4 + 8);  // mbarriers (up to 8 D slots)
   static constexpr int CB = BAR + 8 * (2 * SR_NS + 16) + 16;   // async collector: [SR_CNB][K NV] doubles + SR_CNB mbarriers
   static constexpr int SMEM = CB;
-  static constexpr int SMEM_ACOL = CB + SR_CNB * (4 * SR_CPC / 2) * NV * 8 + SR_CNB * 8;
-  static_assert(P <= 4 && (32 % NV) == 0 && P * NPR <= 4, "SR panel shape (collector buffers hold 2P <= 8 values per CTA)");
+  static constexpr int SMEM_ACOL = CB + SR_CNB * (4 * SR_CPC / 2) * 4 * 8 + SR_CNB * 8;   // K NV <= 320
+  static_assert(P <= 4 && (32 % NV) == 0 && P * NPR <= 4 && ROWB % 16 == 0, "SR panel shape (collector buffers hold 2P <= 8 values per CTA)");
 };
 
 struct SrArgs {
@@ -210,14 +218,35 @@ __device__ __forceinline__ void sr_tm_ld(uint32_t ta, uint32_t (&v)[32]) {
 __device__ __forceinline__ void sr_tm_wait_ld(uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" : SR_RW32(v) :: "memory");
 }
+// 24-word forms (12 doubles per thread and panel): x16 + x8
+__device__ __forceinline__ void sr_tm_st24(uint32_t ta, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               ::"r"(ta + 16), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]),
+               "r"(v[23]) : "memory");
+}
+__device__ __forceinline__ void sr_tm_ld24(uint32_t ta, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]) : "r"(ta) : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23])
+               : "r"(ta + 16) : "memory");
+}
 __device__ __forceinline__ void sr_tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-template <int P, int D, bool TRACE, bool TM, int NG, int NPR, bool ACOL>
-__global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrArgs F) {
-  using L = SrLayout<P, NPR>;
+template <int P, int D, bool TRACE, bool TM, int NG, int NPR, bool ACOL, int CW>
+__global__ void __launch_bounds__(CW * 32 + 32, 1) sr_sweep_kernel(const SrArgs F) {
+  using L = SrLayout<P, NPR, CW>;
   constexpr int NV = L::NV;
+  constexpr int THREADS = CW * 32, COLL = THREADS;   // consumer threads; the collector warp follows
   constexpr int NE = P * NPR * 4;   // exps per thread and panel (rows x pairs x sets x 2 columns)
-  static_assert(!TM || NE == 16, "TMEM slot = 32 columns");
+  constexpr int SW = 2 * NE;        // TMEM columns per parked panel
+  static_assert(!TM || NE == 16 || NE == 12, "TMEM slot = 32 or 24 columns");
   extern __shared__ __align__(128) char smem[];
   char* ring = smem + L::RING;
   double* red = reinterpret_cast<double*>(smem + L::RED);
@@ -230,12 +259,12 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
   int* s_cnt = reinterpret_cast<int*>(wfree + D + 1);               // [SR_NR] warps done with a panel
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cnt + SR_NR);     // TMEM base address (TM)
   static_assert(SR_NS + 2 * D + 1 + SR_NR / 2 + 1 <= 2 * SR_NS + 16 && SR_NR >= D + 1 && 2 * D <= SR_NSLOT, "SR slots");
-  // TM: 3 consumer warps share a lane quarter, each parks D panels x 32 columns
-  static_assert(!TM || 3 * 32 * D <= 512, "TMEM slots");
+  // TM: up to (CW + 3) / 4 consumer warps share a lane quarter, each parks D panels x SW columns
+  static_assert(!TM || ((CW + 3) / 4) * SW * D <= 512, "TMEM slots");
   load_table(reinterpret_cast<double*>(smem));
   if (threadIdx.x == 0) {
     for (int s = 0; s < SR_NS; ++s) mbar_init(full + s, 1);
-    for (int s = 0; s < D; ++s) { mbar_init(wready + s, 1); mbar_init(wfree + s, SR_CW); }
+    for (int s = 0; s < D; ++s) { mbar_init(wready + s, 1); mbar_init(wfree + s, CW); }
     *s_abort = 0;
     for (int i = 0; i < SR_NR; ++i) s_cnt[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -263,8 +292,8 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
       TRACE && F.trace && (c == 0 || c == G - 1) ? F.trace + (c == 0 ? 0 : 8 * 4096) : nullptr;
   if (!TRACE || npl > 4096) trace = nullptr;
 
-  if (threadIdx.x >= SR_COLL && F.dbg_nowait) return;
-  if (threadIdx.x >= SR_COLL) {  // ------------------------- collector warp -------------------------
+  if (threadIdx.x >= COLL && F.dbg_nowait) return;
+  if (threadIdx.x >= COLL) {  // ------------------------- collector warp -------------------------
     // Layout of a panel's partials: [CTA c][v = 2 r + k], the group's K CTAs contiguous.  Lane
     // l loads 16-byte pairs at doubles 2 l + 64 jj: values v0 = 2 (l % LPC), v0 + 1 of CTA
     // CPL jj + l / LPC (LPC = NV / 2 lanes per CTA), so lanes l ^ LPC, l ^ 2 LPC, ... hold the
@@ -296,8 +325,8 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
     // buffer t % SR_CNB, completion on that buffer's mbarrier (32 lane arrivals per issue);
     // loads of the next SR_LEAD panels are in flight while panel t is finalized, so the
     // collector is not limited to one L2 round trip per panel
-    static_assert(!ACOL || NG == 2, "async collector buffers are sized for two row groups");
-    constexpr int KNV = (4 * SR_CPC / 2) * NV;                 // buffer doubles (K <= 80)
+    static_assert(!ACOL || NG >= 2, "async collector buffers are sized for row groups");
+    constexpr int KNV = (4 * SR_CPC / NG) * NV;                // buffer doubles (K <= 160 / NG)
     double* cb = reinterpret_cast<double*>(smem + L::CB);
     uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + L::CB + SR_CNB * KNV * 8);
     uint32_t cph = 0;                                           // wait parity per buffer
@@ -428,7 +457,8 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
   // Column group of this warp.  Warp w issues on SMSP w % 4; the collector (warp 11) shares
   // SMSP 3 with warps 3 and 7, so warp 7 takes the LAST column group, which is the least
   // filled when W < NPR x 704, leaving the collector issue slots.
-  const int cgrp = warp == 7 ? SR_CW - 1 : (warp == SR_CW - 1 ? 7 : warp);
+  constexpr int WS = CW - 4;   // last consumer warp on the collector's SMSP
+  const int cgrp = warp == WS ? CW - 1 : (warp == CW - 1 ? WS : warp);
   const int tcol = cgrp * 32 + lane;
   // column pair u of this thread: local columns jt[u], jt[u] + 1 (n and W even: pairs are whole)
   int jt[NPR];
@@ -436,7 +466,7 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
   double na[2], nb[2][NPR][2], acc[2][NPR][2];
 #pragma unroll
   for (int u = 0; u < NPR; ++u) {
-    jt[u] = 2 * tcol + 2 * SR_THREADS * u;
+    jt[u] = 2 * tcol + 2 * THREADS * u;
     has[u] = j0 + jt[u] < j1;
   }
 #pragma unroll
@@ -456,7 +486,12 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
     const int rows = (int)(nr - li0 < P ? nr - li0 : P);
     char* dst = ring + slot * L::SLOT;
     uint64_t* bar = full + slot;
-    if (rows < P) {  // last, partial panel: plain loads (a bulk copy would read past nr)
+    if (F.dbg_nowait == 2) {   // debug timing: no C data (the slot keeps stale contents)
+      mbar_arrive(bar);
+      return;
+    }
+    if (rows < P || P * 8 < 16) {  // last, partial panel (a bulk copy would read past nr) or a
+                                   // header below the bulk copy's 16-byte minimum: plain loads
       int64_t* hdr = reinterpret_cast<int64_t*>(dst);
 #pragma unroll
       for (int r = 0; r < P; ++r) hdr[r] = F.shift[li0 + (r < rows ? r : rows - 1)];
@@ -513,13 +548,13 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
     // refills the ring slot every warp has now read -- no CTA-wide barrier, so warps drift
     // apart and one warp's reduction latency overlaps the others' exps.
     const double y = warp_transpose_sum<NV>(rs, lane);
-    double* rb = red + pr * (SR_CW * NV);
+    double* rb = red + pr * (CW * NV);
     if ((lane & (32 / NV - 1)) == 0) rb[warp * NV + lane / (32 / NV)] = y;
     __syncwarp();
     int last = 0;
     if (lane == 0) {
       __threadfence_block();
-      last = atomicAdd(s_cnt + pr, 1) == SR_CW - 1;
+      last = atomicAdd(s_cnt + pr, 1) == CW - 1;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
@@ -532,7 +567,7 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
         const volatile double* vb = rb;
         double t = vb[lane];
 #pragma unroll
-        for (int w = 1; w < SR_CW; ++w) t += vb[w * NV + lane];
+        for (int w = 1; w < CW; ++w) t += vb[w * NV + lane];
         const unsigned long long bits = ((unsigned long long)__double_as_longlong(t) & 0x7fffffffffffffffull) | pp;
         st_relaxed_u64(F.part + (ps * G + c) * NV + lane, bits);
         if (TRACE && trace && lane == 0) trace[p * 8] = clock64();
@@ -579,30 +614,34 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
   if constexpr (TM) {
     // exps parked in TMEM: panel p is computed in registers, stored to slot p % D, and
     // reloaded for the fold D - 1 panels later (the load is issued before the next compute)
-    const uint32_t tw = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 32 * D);
+    const uint32_t tw = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * SW * D);
     double E[P][NPR][2][2];
     uint32_t Fv[32];
     for (int p = 0; p < npl + D - 1; ++p) {
       const int q = p - (D - 1);
       sr_tm_wait_st();   // the previous panel's store (q <= p - 2 was stored before it)
-      if (q >= 0) sr_tm_ld(tw + 32 * (q % D), Fv);
+      if (q >= 0) {
+        if constexpr (NE == 16) sr_tm_ld(tw + SW * (q % D), Fv);
+        else sr_tm_ld24(tw + SW * (q % D), Fv);
+      }
       if (p < npl) {
         compute(p, E);
         uint32_t ev[32];
         const double* Ef = &E[0][0][0][0];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          ev[2 * i] = (uint32_t)__double2loint(Ef[i]);
-          ev[2 * i + 1] = (uint32_t)__double2hiint(Ef[i]);
+          ev[2 * i] = i < NE ? (uint32_t)__double2loint(Ef[i]) : 0u;
+          ev[2 * i + 1] = i < NE ? (uint32_t)__double2hiint(Ef[i]) : 0u;
         }
-        sr_tm_st(tw + 32 * (p % D), ev);
+        if constexpr (NE == 16) sr_tm_st(tw + SW * (p % D), ev);
+        else sr_tm_st24(tw + SW * (p % D), ev);
       }
       if (q >= 0) {
         sr_tm_wait_ld(Fv);
         double Eq[P][NPR][2][2];
         double* Ef = &Eq[0][0][0][0];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) Ef[i] = __hiloint2double((int)Fv[2 * i + 1], (int)Fv[2 * i]);
+        for (int i = 0; i < NE; ++i) Ef[i] = __hiloint2double((int)Fv[2 * i + 1], (int)Fv[2 * i]);
         accumulate(q, Eq, q % D, (uint32_t)((q / D) & 1));
       }
     }
@@ -635,7 +674,7 @@ __global__ void __launch_bounds__(SR_THREADS + 32, 1) sr_sweep_kernel(const SrAr
     }
   if (TM) {   // consumers only (the collector has returned): free TMEM after every warp's last load
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    asm volatile("bar.sync 1, %0;" ::"n"(SR_THREADS) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }
@@ -651,7 +690,7 @@ static char sr_variant() {
   static char v = 0;
   if (!v) {
     const char* e = getenv("LEANOT_SR_VAR");
-    v = (e && (e[0] == 't' || e[0] == 'r' || e[0] == 'h')) ? e[0] : 'g';
+    v = (e && (e[0] == 't' || e[0] == 'r' || e[0] == 'h' || e[0] == 'w')) ? e[0] : 'g';
   }
   return v;
 }
@@ -684,28 +723,29 @@ static unsigned long long* g_sr_trace = nullptr;
 // every variant: 2 P <= 8)
 static int64_t sr_ws_doubles(int G) { return (int64_t)SR_NSLOT * G * 8 + 2; }
 
-template <int P, int D, bool TM, int NG, int NPR, bool ACOL>
+template <int P, int D, bool TM, int NG, int NPR, bool ACOL, int CW = SR_CW>
 static int launch_sr_variant(const leanot_dxg_plan_t& Pl, const CostView& cv, cudaStream_t st) {
-  using Lay = SrLayout<P, NPR>;
+  using Lay = SrLayout<P, NPR, CW>;
+  constexpr int NT = CW * 32 + 32;
   constexpr int SMEM = ACOL ? Lay::SMEM_ACOL : Lay::SMEM;
   const int G = num_sms();
   if (G % NG != 0 || G / NG > 4 * SR_CPC / NG) return LEANOT_EINVAL;
   const int K = G / NG;
   const int64_t W = (((Pl.n + K - 1) / K) + 1) & ~int64_t(1);
-  if (W > NPR * SR_WMAX) return LEANOT_EINVAL;
+  if (W > NPR * 2 * CW * 32) return LEANOT_EINVAL;
   const int64_t gcol_off = (sr_ws_doubles(G) + 15) & ~int64_t(15);
   const int64_t need = NG > 1 ? gcol_off + (int64_t)NG * 2 * Pl.n : sr_ws_doubles(G);
   if (need > (int64_t)Pl.splits * 2 * Pl.n) return LEANOT_EINVAL;
-  auto kern = g_sr_trace ? sr_sweep_kernel<P, D, true, TM, NG, NPR, ACOL> : sr_sweep_kernel<P, D, false, TM, NG, NPR, ACOL>;
+  auto kern = g_sr_trace ? sr_sweep_kernel<P, D, true, TM, NG, NPR, ACOL, CW> : sr_sweep_kernel<P, D, false, TM, NG, NPR, ACOL, CW>;
   static bool attr = false;
   if (!attr) {
-    for (auto kk : {sr_sweep_kernel<P, D, true, TM, NG, NPR, ACOL>, sr_sweep_kernel<P, D, false, TM, NG, NPR, ACOL>})
+    for (auto kk : {sr_sweep_kernel<P, D, true, TM, NG, NPR, ACOL, CW>, sr_sweep_kernel<P, D, false, TM, NG, NPR, ACOL, CW>})
       if (cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
         return LEANOT_EINVAL;
     if (cudaFuncSetAttribute(fused_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_BYTES) != cudaSuccess)
       return LEANOT_EINVAL;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SR_THREADS + 32, SMEM) != cudaSuccess || occ < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, SMEM) != cudaSuccess || occ < 1)
       return LEANOT_EINVAL;
     attr = true;
   }
@@ -725,7 +765,7 @@ static int launch_sr_variant(const leanot_dxg_plan_t& Pl, const CostView& cv, cu
   F.trace = g_sr_trace;
   {
     const char* e = getenv("LEANOT_SR_DBG_NOWAIT");
-    F.dbg_nowait = (e && e[0] == '1') ? 1 : 0;
+    F.dbg_nowait = e ? atoi(e) : 0;
   }
   // generation-0 slots must read as "not ready": sign bit set (0xff bytes), error flag 0
   cudaMemsetAsync(F.part, 0xff, (size_t)(sr_ws_doubles(G) - 2) * 8, st);
@@ -733,7 +773,7 @@ static int launch_sr_variant(const leanot_dxg_plan_t& Pl, const CostView& cv, cu
   cudaLaunchConfig_t lc;
   memset(&lc, 0, sizeof(lc));
   lc.gridDim = dim3(G);
-  lc.blockDim = dim3(SR_THREADS + 32);
+  lc.blockDim = dim3(NT);
   lc.dynamicSmemBytes = SMEM;
   lc.stream = st;
   cudaLaunchAttribute at[1];
@@ -764,6 +804,10 @@ static int try_sr_sweep(const leanot_dxg_plan_t& P, cudaStream_t st, bool force 
   const CostView cv = make_view(P.cost);
   if (!tma_ok(cv) || (!force && (!sr_enabled() || P.n < sr_min_n()))) return LEANOT_EINVAL;
   const char v = sr_variant();
+  if (v == 'w') {
+    const int rc = launch_sr_variant<1, 5, true, 4, 3, true, 15>(P, cv, st);
+    if (rc != LEANOT_EINVAL) return rc;
+  }
   if (v == 'g' || v == 'h') {
     const int rc = v == 'g' ? launch_sr_variant<2, 5, true, 2, 2, true>(P, cv, st)
                             : launch_sr_variant<2, 5, true, 2, 2, false>(P, cv, st);
