@@ -46,6 +46,8 @@
 // the consumer instruction stream, not the exchange, is what binds.
 // Included by leanot_lib.cu after leanot_fused.cu (mbarrier / bulk-copy helpers).
 
+#include <type_traits>
+
 namespace leanot {
 
 constexpr int SR_CW = 11;                    // consumer warps
@@ -236,6 +238,24 @@ __device__ __forceinline__ void sr_tm_ld24(uint32_t ta, uint32_t (&v)[32]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23])
                : "r"(ta + 16) : "memory");
+}
+
+// 16 doubles per thread as 32 TMEM columns, the 64-bit halves split / joined inside the asm so
+// the compiler keeps the doubles in their register pairs (no moves); the load waits for its
+// own completion before the joins
+__device__ __forceinline__ void sr_tm_st16d(uint32_t ta, const double (&e)[16]) {
+  asm volatile("{\n\t.reg .b32 t<32>;\n\t"
+      "mov.b64 {t0, t1}, %1;\n\t""mov.b64 {t2, t3}, %2;\n\t""mov.b64 {t4, t5}, %3;\n\t""mov.b64 {t6, t7}, %4;\n\t""mov.b64 {t8, t9}, %5;\n\t""mov.b64 {t10, t11}, %6;\n\t""mov.b64 {t12, t13}, %7;\n\t""mov.b64 {t14, t15}, %8;\n\t""mov.b64 {t16, t17}, %9;\n\t""mov.b64 {t18, t19}, %10;\n\t""mov.b64 {t20, t21}, %11;\n\t""mov.b64 {t22, t23}, %12;\n\t""mov.b64 {t24, t25}, %13;\n\t""mov.b64 {t26, t27}, %14;\n\t""mov.b64 {t28, t29}, %15;\n\t""mov.b64 {t30, t31}, %16;\n\t"
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11, t12, t13, t14, t15, t16, t17, t18, t19, t20, t21, t22, t23, t24, t25, t26, t27, t28, t29, t30, t31};\n\t}"
+      ::"r"(ta), "d"(e[0]), "d"(e[1]), "d"(e[2]), "d"(e[3]), "d"(e[4]), "d"(e[5]), "d"(e[6]), "d"(e[7]), "d"(e[8]), "d"(e[9]), "d"(e[10]), "d"(e[11]), "d"(e[12]), "d"(e[13]), "d"(e[14]), "d"(e[15]) : "memory");
+}
+__device__ __forceinline__ void sr_tm_ld16d(uint32_t ta, double (&e)[16]) {
+  asm volatile("{\n\t.reg .b32 t<32>;\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11, t12, t13, t14, t15, t16, t17, t18, t19, t20, t21, t22, t23, t24, t25, t26, t27, t28, t29, t30, t31}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;\n\t"
+      "mov.b64 %0, {t0, t1};\n\t""mov.b64 %1, {t2, t3};\n\t""mov.b64 %2, {t4, t5};\n\t""mov.b64 %3, {t6, t7};\n\t""mov.b64 %4, {t8, t9};\n\t""mov.b64 %5, {t10, t11};\n\t""mov.b64 %6, {t12, t13};\n\t""mov.b64 %7, {t14, t15};\n\t""mov.b64 %8, {t16, t17};\n\t""mov.b64 %9, {t18, t19};\n\t""mov.b64 %10, {t20, t21};\n\t""mov.b64 %11, {t22, t23};\n\t""mov.b64 %12, {t24, t25};\n\t""mov.b64 %13, {t26, t27};\n\t""mov.b64 %14, {t28, t29};\n\t""mov.b64 %15, {t30, t31};\n\t"
+      "}"
+      : "=d"(e[0]), "=d"(e[1]), "=d"(e[2]), "=d"(e[3]), "=d"(e[4]), "=d"(e[5]), "=d"(e[6]), "=d"(e[7]), "=d"(e[8]), "=d"(e[9]), "=d"(e[10]), "=d"(e[11]), "=d"(e[12]), "=d"(e[13]), "=d"(e[14]), "=d"(e[15]) : "r"(ta) : "memory");
 }
 __device__ __forceinline__ void sr_tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -514,7 +534,14 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) sr_sweep_kernel(const SrArgs 
   // partial-sum slot ps = p % NSLOT with generation parity pp
   int pr = 0, ps = 0;
   unsigned long long pp = 0;
-  auto compute = [&](int p, double (&E)[P][NPR][2][2]) {
+  // warps whose every lane has all its column pairs (all but the tail warps) skip the
+  // per-pair selects; both forms add the same terms in the same order
+  bool allhas = true;
+#pragma unroll
+  for (int u = 0; u < NPR; ++u) allhas = allhas && has[u];
+  const bool warp_full = __all_sync(0xffffffffu, allhas);
+  auto compute_f = [&](int p, double (&E)[P][NPR][2][2], auto fullc) {
+    constexpr bool fw = decltype(fullc)::value;
     sr_wait(full + s, ph, s_abort);
     const char* st = ring + s * L::SLOT;
     double rs[NV];
@@ -536,7 +563,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) sr_sweep_kernel(const SrArgs 
           for (int k = 0; k < 2; ++k) {
             E[r][u][k][0] = texp(tb, fma(na[k], cc.x, nb[k][u][0]), ml);
             E[r][u][k][1] = texp(tb, fma(na[k], cc.y, nb[k][u][1]), ml);
-            rs[r * 2 + k] += has[u] ? E[r][u][k][0] + E[r][u][k][1] : 0.0;
+            rs[r * 2 + k] += (fw || has[u]) ? E[r][u][k][0] + E[r][u][k][1] : 0.0;
           }
         }
       }
@@ -575,6 +602,10 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) sr_sweep_kernel(const SrArgs 
     }
     if (++pr == SR_NR) pr = 0;
     if (++ps == SR_NSLOT) { ps = 0; pp ^= 1ull << 63; }
+  };
+  auto compute = [&](int p, double (&E)[P][NPR][2][2]) {
+    if (warp_full) compute_f(p, E, std::true_type{});
+    else compute_f(p, E, std::false_type{});
   };
   // fold panel q (exps E, slot ds = q % D, wready parity wpar) into the column sums
   auto accumulate = [&](int q, const double (&E)[P][NPR][2][2], int ds, uint32_t wpar) {
@@ -620,28 +651,34 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) sr_sweep_kernel(const SrArgs 
     for (int p = 0; p < npl + D - 1; ++p) {
       const int q = p - (D - 1);
       sr_tm_wait_st();   // the previous panel's store (q <= p - 2 was stored before it)
-      if (q >= 0) {
-        if constexpr (NE == 16) sr_tm_ld(tw + SW * (q % D), Fv);
-        else sr_tm_ld24(tw + SW * (q % D), Fv);
+      if constexpr (NE != 16) {
+        if (q >= 0) sr_tm_ld24(tw + SW * (q % D), Fv);
       }
       if (p < npl) {
         compute(p, E);
-        uint32_t ev[32];
-        const double* Ef = &E[0][0][0][0];
+        if constexpr (NE == 16) {
+          sr_tm_st16d(tw + SW * (p % D), reinterpret_cast<const double(&)[16]>(E));
+        } else {
+          uint32_t ev[32];
+          const double* Ef = &E[0][0][0][0];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          ev[2 * i] = i < NE ? (uint32_t)__double2loint(Ef[i]) : 0u;
-          ev[2 * i + 1] = i < NE ? (uint32_t)__double2hiint(Ef[i]) : 0u;
+          for (int i = 0; i < 16; ++i) {
+            ev[2 * i] = i < NE ? (uint32_t)__double2loint(Ef[i]) : 0u;
+            ev[2 * i + 1] = i < NE ? (uint32_t)__double2hiint(Ef[i]) : 0u;
+          }
+          sr_tm_st24(tw + SW * (p % D), ev);
         }
-        if constexpr (NE == 16) sr_tm_st(tw + SW * (p % D), ev);
-        else sr_tm_st24(tw + SW * (p % D), ev);
       }
       if (q >= 0) {
-        sr_tm_wait_ld(Fv);
         double Eq[P][NPR][2][2];
-        double* Ef = &Eq[0][0][0][0];
+        if constexpr (NE == 16) {
+          sr_tm_ld16d(tw + SW * (q % D), reinterpret_cast<double(&)[16]>(Eq));
+        } else {
+          sr_tm_wait_ld(Fv);
+          double* Ef = &Eq[0][0][0][0];
 #pragma unroll
-        for (int i = 0; i < NE; ++i) Ef[i] = __hiloint2double((int)Fv[2 * i + 1], (int)Fv[2 * i]);
+          for (int i = 0; i < NE; ++i) Ef[i] = __hiloint2double((int)Fv[2 * i + 1], (int)Fv[2 * i]);
+        }
         accumulate(q, Eq, q % D, (uint32_t)((q / D) & 1));
       }
     }
