@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the config-4 shard (FP64-bound path) timing")
     ap.add_argument("--no-tte", action="store_true", help="skip the config-1 time-to-eps run")
     return ap.parse_args()
 
@@ -246,6 +247,51 @@ def time_to_eps_config1():
             "reference_seconds_survey_4workers": 93.0}
 
 
+def fp64_path_config4(iters=2):
+    """BASELINE config 4's per-GPU work (one 1/8 row shard of n=1e6 3-D points, cost on the fly)
+    timed in this run: the FP64-bound path's roofline (north_star: >= 70 % of the FP64 roofline
+    for on-the-fly C).  Same engine calls as tools/bench_configs.py config4."""
+    import torch
+    from paper_2511_11359_b200 import core, dxg
+    from paper_2511_11359_b200.engine import DxgEngine, shard_rows
+    n, shards = 1_000_000, 8
+    rng = np.random.default_rng(4)
+    f = rng.random((n, 3))
+    f[0], f[1] = 0.0, 1.0            # cube corners: raw sup = 3 by construction
+    k = core.ColorKernel(f, 2, scale=3.0)
+    r0, r1 = shard_rows(n, shards, 0)
+    k.row0, k.row1 = r0, r1
+    w1, w2 = rng.random(n), rng.random(n)
+    eng = DxgEngine(k, w1 / w1.sum(), w2 / w2.sum(), dxg.params_tuned(1e-7).with_overrides(tau_mu=0.05))
+    eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
+    eng.sweep()
+    eng.update()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(iters):
+        eng.sweep()
+        eng.update()
+    e1.record(st)
+    torch.cuda.synchronize()
+    per_iter = e0.elapsed_time(e1) / 1e3 / iters
+    elems = n * (r1 - r0)
+    executed = 2 * (3 + 2 * 8)   # per element and iteration: 2 passes x (3-term dot + 2 sets x (x' + 7 exp))
+    peak = 17.07e12              # builder DFMA microbenchmark at 1965 MHz (profiles/r01_microbench.md)
+    return {"what": "BASELINE config 4 per-GPU work: one 1/8 row shard of n=1e6 3-D points (cost on the fly, "
+                    "expanded form), DXG iteration, measured in this run (CUDA events)",
+            "rows": r1 - r0, "n": n, "iters": iters, "seconds_per_iteration": per_iter,
+            "fp64_instr_per_s_executed": executed * elems / per_iter,
+            "frac_executed": executed * elems / per_iter / peak,
+            "frac_survey_count": 47 * elems / per_iter / peak,
+            "peak_fp64_instr_per_s": peak,
+            "peak_source": "builder DFMA microbenchmark (tools/microbench/fp64_bench.cu, 17.07e12/s at 1965 MHz); "
+                           "MEASURED_PEAKS.json has no FP64 entry",
+            "definitions": "executed: 38 FP64 instructions per element and iteration the two-pass expanded-form "
+                           "kernels issue; survey: SURVEY.md 8(d)'s 47 per element (libdevice exp count)"}
+
+
 def run_b200(args):
     import torch
     world, rank, local, group = init_dist(args)
@@ -403,6 +449,11 @@ def run_b200(args):
                     "instance": "BASELINE config 3 (n=1e5 stored C, tuned + tau_mu=0.05)", "eps": hits}
             except Exception as e:  # report, do not hide
                 line["time_to_eps_n1e5_recorded"] = {"error": repr(e)}
+    if rank == 0 and world == 1 and not args.no_fp64:
+        try:
+            line["fp64_path"] = fp64_path_config4()
+        except Exception as e:  # report, do not hide
+            line["fp64_path"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_reference(n, args.seed, steps=2, warmup=1)
     if rank == 0:
