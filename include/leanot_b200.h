@@ -165,8 +165,9 @@ int leanot_dxg_prepare(const leanot_dxg_plan_t* plan, double a, double s, double
 /* stored cost, plain iteration: one persistent launch, pass B re-reads C from L2
  * (csrc/leanot_fused.cu; experimental, slower than the two-pass kernels as of r01) */
 #define LEANOT_SWEEP_FUSED 8
-/* stored cost, plain iteration, n <= 704 x #SMs: SINGLE_READ runs the single-read, single-exp
- * sweep (csrc/leanot_sr.cu; one read of C, one exp per element and weight set; opt-in, slower
+/* stored cost, plain iteration, n <= 1408 x #SMs / 2 (column tiles of the 2-group form; other
+ * plans fall back to passes A + B): SINGLE_READ runs the single-read, single-exp sweep
+ * (csrc/leanot_sr.cu; one read of C, one exp per element and weight set; opt-in, not faster
  * than the two-pass sweep at n = 1e5 as of r02 -- the default when LEANOT_SR=1 and n >= 32768);
  * TWO_PASS forces passes A + B */
 #define LEANOT_SWEEP_TWO_PASS 16
