@@ -178,3 +178,50 @@ def test_single_read_fixup_of_flagged_rows():
     assert np.all(np.isfinite(c0))
     assert rel_err(c0, c1) <= 1e-12
     assert np.max(np.abs(h0 - h1)) <= 1
+
+
+_SR_SOLVE = r"""
+import json, sys
+import numpy as np
+import torch
+from paper_2511_11359_b200 import _lib, core, dxg
+n = 4096
+k = core.HashKernel(n, seed=0)
+rng = np.random.default_rng(1)
+rw, cw = rng.random(n), rng.random(n)
+r, c = core.Histogram(rw / rw.sum()), core.Histogram(cw / cw.sum())
+prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+tr = torch.zeros(2 * 8 * 4096, dtype=torch.int64, device="cuda")
+_lib.lib().leanot_debug_sr_trace(tr.data_ptr())   # proves the single-read kernel ran
+sol = dxg.solve(k, r, c, prm, dxg.Termination(eps=1e-4), log_stride=25, dense_cap=0)
+torch.cuda.synchronize()
+_lib.lib().leanot_debug_sr_trace(None)
+traj = [[p.iter, p.primal, p.dual, p.gap, p.col_infeas_l1, p.s] for p in sol.trajectory]
+np.savez(sys.argv[1], traj=np.array(traj), delta=sol.state.mu.delta, iterations=sol.iterations,
+         converged=sol.converged, sr_stamps=int((tr != 0).sum().item()))
+"""
+
+
+def test_single_read_solve_matches_reference_iteration_count(tmp_path):
+    """The config-3 instance family at n = 4096 solved to eps = 1e-4 with every plain iteration
+    on the single-read sweep (LEANOT_SR=1, LEANOT_SR_MIN_N=0, persistent path off; evaluation
+    sweeps stay two-pass): the reference's 12,950 iterations and its logged primal/dual values
+    within 1e-8, as the default path (tests/test_gpu_configs.py).  Runs in a subprocess because the
+    library reads these switches once per process."""
+    import os
+    import subprocess
+    import sys
+    from helpers import load
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "sr_solve.npz"
+    env = dict(os.environ, LEANOT_SR="1", LEANOT_SR_MIN_N="0", LEANOT_PERSIST="0", PYTHONPATH=root)
+    subprocess.run([sys.executable, "-c", _SR_SOLVE, str(out)], check=True, env=env, cwd=root, timeout=600)
+    got = np.load(out)
+    d = load("hash4096_eps1e-4")
+    assert int(got["sr_stamps"]) > 0
+    assert bool(got["converged"]) == bool(d["converged"])
+    assert int(got["iterations"]) == int(d["iterations"]) == 12950
+    ref = d["traj"]
+    assert got["traj"].shape == ref.shape and np.array_equal(got["traj"][:, 0], ref[:, 0])
+    assert rel_err(got["traj"][:, 1], ref[:, 1]) <= 1e-8 and rel_err(got["traj"][:, 2], ref[:, 2]) <= 1e-8
+    assert rel_err(got["delta"], d["delta"]) <= 1e-8
