@@ -449,6 +449,30 @@ def run_b200(args):
                     "instance": "BASELINE config 3 (n=1e5 stored C, tuned + tau_mu=0.05)", "eps": hits}
             except Exception as e:  # report, do not hide
                 line["time_to_eps_n1e5_recorded"] = {"error": repr(e)}
+    if world == 1 and not args.no_fp64:
+        # the opt-in single-read sweep (one read of C, 2 exps per element) on the same engine,
+        # timed after the headline region: what the north-star single-read design measures here
+        try:
+            for _ in range(2):
+                eng.sweep(single_read=True)
+                eng.update()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for _ in range(5):
+                eng.sweep(single_read=True)
+                eng.update()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            t_sr = ev0.elapsed_time(ev1) / 1e3 / 5
+            line["single_read"] = {
+                "what": "opt-in single-read sweep (csrc/leanot_sr.cu, default variant g) + update, 5 iterations "
+                        "after the headline region, CUDA events",
+                "ms_per_iteration": 1e3 * t_sr, "iters_per_s": 1.0 / t_sr,
+                "hbm_frac_one_read": bytes_alg / t_sr / 1e9 / peak,
+                "limiter": "consumer instruction stream (profiles/r02/sr_instr_mix.md); not the default path"}
+        except Exception as e:  # report, do not hide
+            line["single_read"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_fp64:
         try:
             line["fp64_path"] = fp64_path_config4()
