@@ -111,6 +111,39 @@ def test_single_read_iterations_track_two_pass():
     assert a0 == a1 and s0 == s1 and t0 == t1 == 125
 
 
+def test_single_read_tracks_two_pass_at_baseline_size():
+    """BASELINE config 3's shape (n = 1e5, the 80 GB hash matrix, the bench's marginals and
+    parameters, fresh start): 5 DXG iterations on the single-read sweep (the 2-group TMEM form
+    the bench's `single_read` object times) against 5 on the two-pass sweep, same matrix."""
+    import torch
+    from paper_2511_11359_b200 import core, dxg
+    from paper_2511_11359_b200.engine import DxgEngine
+    n = 100_000
+    k = core.HashKernel(n, seed=0)
+    rng = np.random.default_rng(1)
+    r, c = rng.random(n), rng.random(n)
+    r, c = r / r.sum(), c / c.sum()
+    prm = dxg.params_tuned(0.0).with_overrides(tau_mu=0.05)
+    states, cols = [], []
+    for mode in ("sr", "two"):
+        eng = DxgEngine(k, r, c, prm)
+        eng.load_state(np.zeros(n), np.zeros(n), 0.0, 0.0, 0, fresh=True)
+        for _ in range(5):
+            _sweep(eng, mode)
+            eng.update()
+        _sweep(eng, mode)
+        torch.cuda.synchronize()
+        assert mode != "sr" or _sr_ran(eng)
+        cols.append(eng.col.cpu().numpy().copy())
+        states.append(eng.read_state())
+        del eng
+        torch.cuda.empty_cache()
+    (d0, b0, a0, s0, t0), (d1, b1, a1, s1, t1) = states
+    assert rel_err(cols[0], cols[1]) <= 1e-12
+    assert rel_err(d0, d1) <= 1e-11 and rel_err(b0, b1) <= 1e-11
+    assert a0 == a1 and s0 == s1 and t0 == t1 == 5
+
+
 def test_single_read_is_opt_in():
     """engine.sweep() with no mode runs the two-pass sweep (the single-read kernel is opt-in:
     LEANOT_SR=1 or single_read=True); forcing it leaves its slots written."""
