@@ -842,6 +842,12 @@ static int launch_sr_variant(const leanot_dxg_plan_t& Pl, const CostView& cv, cu
   {
     const char* e = getenv("LEANOT_SR_DBG_NOWAIT");
     F.dbg_nowait = e ? atoi(e) : 0;
+    static bool warned = false;
+    if (F.dbg_nowait && !warned) {
+      fprintf(stderr, "leanot: LEANOT_SR_DBG_NOWAIT=%d -- single-read sweeps run in a timing-only debug mode "
+                      "and their results are WRONG\n", F.dbg_nowait);
+      warned = true;
+    }
   }
   // generation-0 slots must read as "not ready": sign bit set (0xff bytes), error flag 0
   cudaMemsetAsync(F.part, 0xff, (size_t)(sr_ws_doubles(G) - 2) * 8, st);
