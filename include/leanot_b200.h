@@ -288,6 +288,12 @@ int leanot_round_polytope(double* m, int64_t n, int64_t ld, const double* r, con
 /* out[0] = <C, P> (rounded_cost, dxg.py:471); scratch >= 1024 doubles */
 int leanot_plan_cost(const leanot_cost_t* cost, const double* P, int64_t ld, double* out, double* scratch,
                      void* stream);
+/* pdxg_reference_step (dxg.py:494-521, the dense equivalence oracle of the reference), n <= dense cap:
+ * out = z - lse_rows(z) with z = decay lp - tau (C + two_sup d[None, :]) (dxg.py:508-509, :514-515;
+ * out must not alias lp), and col = r @ exp(M) (dxg.py:505-506, :511-512) */
+int leanot_pdxg_rows(const leanot_cost_t* cost, const double* lp, int64_t ld, double decay, double tau, double two_sup,
+                     const double* d, double* out, void* stream);
+int leanot_pdxg_colsum(const double* M, int64_t n, int64_t ld, const double* r, double* col, void* stream);
 
 /* ---- separable GridKernel path, O(n^1.5) ---------------
  * C_ij = (f(|dr|) + f(|dc|))/scale factorizes, so each n^2 LSE is two 1-D LSE convolutions.

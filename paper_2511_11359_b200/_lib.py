@@ -113,6 +113,8 @@ def lib():
         "leanot_materialize_plan": ([C.POINTER(CostT), dbl, vp, vp, vp, vp, i64, vp], C.c_int),
         "leanot_round_polytope": ([vp, i64, i64, vp, vp, vp, vp], C.c_int),
         "leanot_plan_cost": ([C.POINTER(CostT), vp, i64, vp, vp, vp], C.c_int),
+        "leanot_pdxg_rows": ([C.POINTER(CostT), vp, i64, dbl, dbl, dbl, vp, vp, vp], C.c_int),
+        "leanot_pdxg_colsum": ([vp, i64, i64, vp, vp, vp], C.c_int),
         "leanot_grid_sep_ws_doubles": ([C.POINTER(CostT)], i64),
         "leanot_grid_sep_lse": ([C.POINTER(CostT), vp, vp, vp, vp, vp], C.c_int),
         "leanot_grid_sep_colsum": ([C.POINTER(CostT), vp, vp, vp, vp, vp, vp], C.c_int),
@@ -138,7 +140,7 @@ EXPORTS = (
     "leanot_sync", "leanot_bary_prepare", "leanot_bary_sweep", "leanot_bary_update", "leanot_bary_eval",
     "leanot_col_lse_ws_doubles", "leanot_col_lse", "leanot_eta_log_minus", "leanot_sinkhorn_psi", "leanot_eot_dual",
     "leanot_sinkhorn_colmarg", "leanot_ibp_rows", "leanot_materialize_plan", "leanot_round_polytope",
-    "leanot_plan_cost", "leanot_grid_sep_ws_doubles", "leanot_grid_sep_lse", "leanot_grid_sep_colsum", "leanot_grid_sep_lse_eta", "leanot_grid_sep_lse_eta_ws_doubles",
+    "leanot_plan_cost", "leanot_pdxg_rows", "leanot_pdxg_colsum", "leanot_grid_sep_ws_doubles", "leanot_grid_sep_lse", "leanot_grid_sep_colsum", "leanot_grid_sep_lse_eta", "leanot_grid_sep_lse_eta_ws_doubles",
 )
 
 

@@ -127,6 +127,80 @@ struct DotFn {
   }
 };
 
+// Dense primal-dual reference step (pdxg_reference_step, dxg.py:494-521), one row per CTA:
+//   z_ij = decay lp_ij - tau (C_ij + two_sup d_j),  out_ij = z_ij - LSE_j z_ij  (lse_rows, core.py:67-70)
+// exact row max, libdevice exp / log (the reference's np.exp / np.log), fixed reduction order.
+template <class COST>
+__global__ void __launch_bounds__(256) pdxg_rows_kernel(const CostView cv, const double* lp, int64_t ld, double decay,
+                                                        double tau, double two_sup, const double* d, double* out) {
+  __shared__ double red[8];
+  __shared__ double bc;
+  const COST cost(cv);
+  const int64_t n = cv.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const typename COST::Row row = cost.row(i);
+    double mx = -INFINITY;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      // the reference's NumPy operation order, no FMA contraction
+      const double z = __dsub_rn(__dmul_rn(decay, lp[i * ld + j]),
+                                 __dmul_rn(tau, __dadd_rn(cost.eval1(row, j), __dmul_rn(two_sup, d[j]))));
+      out[i * ld + j] = z;
+      mx = fmax(mx, z);
+    }
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < 8; ++w) t = fmax(t, red[w]);
+      bc = t;
+    }
+    __syncthreads();
+    const double m = bc;
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) s += exp(out[i * ld + j] - m);
+    s = warp_sum(s);
+    __syncthreads();
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < 8; ++w) t += red[w];
+      bc = m + log(t);
+    }
+    __syncthreads();
+    const double L = bc;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) out[i * ld + j] -= L;
+    __syncthreads();
+  }
+}
+
+// col_j = sum_i r_i exp(M_ij) in ascending row order (r @ np.exp(M), dxg.py:506, :512)
+__global__ void pdxg_colsum_kernel(const double* M, int64_t n, int64_t ld, const double* r, double* col) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s = fma(r[i], exp(M[i * ld + j]), s);
+    col[j] = s;
+  }
+}
+
+struct PdxgRowsFn {
+  const CostView& cv;
+  const double* lp;
+  int64_t ld;
+  double decay, tau, two_sup;
+  const double* d;
+  double* out;
+  cudaStream_t st;
+  template <class COST>
+  int run() {
+    const int grid = (int)std::min<int64_t>(cv.n, 8192);
+    pdxg_rows_kernel<COST><<<grid, 256, 0, st>>>(cv, lp, ld, decay, tau, two_sup, d, out);
+    return LEANOT_OK;
+  }
+};
+
 }  // namespace leanot
 
 extern "C" {
@@ -176,5 +250,29 @@ int leanot_plan_cost(const leanot_cost_t* cost, const double* P, int64_t ld, dou
   sum_kernel<<<1, 1024, 0, S_(stream)>>>(scratch, nb, out);
   return check_launch("plan_cost");
 }
+
+// pdxg_reference_step's row update (dxg.py:508-509, :514-515): out = z - lse_rows(z),
+// z = decay lp - tau (C + two_sup d[None, :]); out may not alias lp
+int leanot_pdxg_rows(const leanot_cost_t* cost, const double* lp, int64_t ld, double decay, double tau, double two_sup,
+                     const double* d, double* out, void* stream) {
+  LEANOT_TRY(validate_cost(cost));
+  LEANOT_TRY(ensure_init());
+  if (ld < cost->n) { set_error("ld < n"); return LEANOT_EINVAL; }
+  if (lp == out) { set_error("pdxg_rows: out must not alias lp"); return LEANOT_EINVAL; }
+  const CostView cv = make_view(*cost);
+  PdxgRowsFn f{cv, lp, ld, decay, tau, two_sup, d, out, S_(stream)};
+  LEANOT_TRY(LEANOT_DISPATCH_COST(cv, f));
+  return check_launch("pdxg_rows");
+}
+
+// col = r @ exp(M) (dxg.py:505-506, :511-512)
+int leanot_pdxg_colsum(const double* M, int64_t n, int64_t ld, const double* r, double* col, void* stream) {
+  LEANOT_TRY(ensure_init());
+  if (n < 1 || ld < n) { set_error("bad dense matrix"); return LEANOT_EINVAL; }
+  const int grid = (int)std::min<int64_t>((n + 127) / 128, 4096);
+  pdxg_colsum_kernel<<<grid, 128, 0, S_(stream)>>>(M, n, ld, r, col);
+  return check_launch("pdxg_colsum");
+}
+
 
 }  // extern "C"

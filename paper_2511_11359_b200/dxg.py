@@ -568,25 +568,43 @@ def pdxg_init(n: int, cap: int = DENSE_CAP) -> PdxgState:
 
 def pdxg_reference_step(state: PdxgState, kernel: CostKernel, r: Histogram, c: Histogram,
                         params: DxgParams) -> PdxgState:
-    """Dense extragradient step on device tensors (dxg.py:494-521)."""
+    """Dense extragradient step (dxg.py:494-521) on device: the row updates
+    z = decay log_p - tau (C + 2 sup d) minus their row LSEs (`leanot_pdxg_rows`, the cost
+    evaluated on device as in the sweeps) and the column marginals r @ exp(.)
+    (`leanot_pdxg_colsum`); the O(n) dual steps are the host functions above."""
     kernel = _dev_kernel(kernel)
     torch = _torch()
     n = kernel.n
     if state.log_p.shape != (n, n):
         raise ValueError("state/kernel size mismatch")
+    if not _holds_all_rows(kernel):
+        raise ValueError("the dense reference step needs every row of the cost")
     dev = kernel.device
-    rw, cw = _to_dev(as_weights(r), dev), as_weights(c)
+    cw = as_weights(c)
     c_tilde = cw + params.alpha / n
     sup = kernel.sup_norm
-    Cm = torch.from_numpy(kernel.materialize()).to(dev)
     decay = 1.0 - params.tau_p * params.eta
-    lp = _to_dev(state.log_p, dev)
-    col_now = (rw @ torch.exp(lp)).cpu().numpy()
-    mu_bar = dual_md_step(state.mu, col_now, Histogram(cw), c_tilde, params, sup)
-    lpb = decay * lp - params.tau_p * (Cm + 2.0 * sup * _to_dev(state.mu.diff(), dev)[None, :])
-    lpb = lpb - torch.logsumexp(lpb, dim=1, keepdim=True)
-    col_bar = (rw @ torch.exp(lpb)).cpu().numpy()
-    mu_next = balance(dual_md_step(state.mu, col_bar, Histogram(cw), c_tilde, params, sup), params.beta)
-    lpn = decay * lp - params.tau_p * (Cm + 2.0 * sup * _to_dev(mu_bar.diff(), dev)[None, :])
-    lpn = lpn - torch.logsumexp(lpn, dim=1, keepdim=True)
-    return PdxgState(mu_next, lpn.cpu().numpy())
+    lib = _lib.lib()
+    with torch.cuda.device(dev):
+        s = _lib.stream_handle()
+        lp = torch.from_numpy(np.ascontiguousarray(state.log_p, dtype=float)).to(dev)
+        rt = _to_dev(as_weights(r), dev)
+        col = torch.empty(n, dtype=torch.float64, device=dev)
+
+        def colsum(M):
+            _lib.check(lib.leanot_pdxg_colsum(M.data_ptr(), n, n, rt.data_ptr(), col.data_ptr(), s), "pdxg_colsum")
+            return col.cpu().numpy()
+
+        def rows(dvec, out):
+            d = _to_dev(np.ascontiguousarray(dvec, dtype=float), dev)
+            _lib.check(lib.leanot_pdxg_rows(kernel.cost_struct(), lp.data_ptr(), n, decay, params.tau_p, 2.0 * sup,
+                                            d.data_ptr(), out.data_ptr(), s), "pdxg_rows")
+            return out
+
+        col_now = colsum(lp)
+        mu_bar = dual_md_step(state.mu, col_now, Histogram(cw), c_tilde, params, sup)
+        buf = torch.empty_like(lp)
+        col_bar = colsum(rows(state.mu.diff(), buf))
+        mu_next = balance(dual_md_step(state.mu, col_bar, Histogram(cw), c_tilde, params, sup), params.beta)
+        lpn = rows(mu_bar.diff(), buf).cpu().numpy()
+    return PdxgState(mu_next, lpn)
